@@ -1,0 +1,236 @@
+/*
+ * hecsolve_c.h -- the C-ABI boundary of the B200 HEC triangular-solve path.
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every entry point returns a status code; on failure the message (and, for
+ * zero pivots, the row/block) is kept in thread-local storage.
+ *
+ *   HEC_OK          0
+ *   HEC_EINVAL      1  std::invalid_argument in the reference
+ *   HEC_ERANGE      2  std::out_of_range
+ *   HEC_ERUNTIME    3  std::runtime_error / CUDA failure / no device
+ *   HEC_EZEROPIVOT  4  hec::ZeroPivotError(row, block)
+ *   HEC_EOVERFLOW   5  std::overflow_error
+ *
+ * Section 1 (hec_tri_*, hec_precond_*, hec_spmv_*, hec_gmres_*) is the device
+ * path: each entry replaces one reference call site (cited per function).
+ * Section 2 (hec_csr_*, hec_prep_*, hec_ilu*, hec_bp_*) exposes the host setup
+ * (bit-identical to the reference) so non-C++ hosts and the test-suite can
+ * drive the whole path through this one library.
+ */
+#ifndef HECSOLVE_C_H
+#define HECSOLVE_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    HEC_OK = 0,
+    HEC_EINVAL = 1,
+    HEC_ERANGE = 2,
+    HEC_ERUNTIME = 3,
+    HEC_EZEROPIVOT = 4,
+    HEC_EOVERFLOW = 5
+};
+
+const char* hec_last_error(void);
+int hec_last_error_row(void);
+int hec_last_error_block(void);
+/* library version string ("hecsolve-b200 <semver> sm_100a") */
+const char* hec_version(void);
+/* 1 if a CUDA device is usable by this process, else 0 (never fails). */
+int hec_device_available(void);
+
+/* ===================== Section 1: device path ========================== */
+
+/* Solve strategies (hec_tri_options.strategy). */
+enum {
+    HEC_STRATEGY_AUTO = 0,
+    HEC_STRATEGY_LEVELS = 1,    /* one launch per level, captured in a CUDA graph  */
+    HEC_STRATEGY_PIPELINE = 2   /* persistent CTA-owned chunk pipeline (default)   */
+};
+
+typedef struct {
+    int strategy;      /* HEC_STRATEGY_*                                        */
+    int ctas;          /* persistent CTAs for PIPELINE; 0 = auto (cost model)   */
+    int threads;       /* threads per CTA; 0 = auto                             */
+    int reserved[5];
+} hec_tri_options;
+
+typedef struct {
+    int n;
+    int nlev;
+    int strategy;        /* strategy actually used                              */
+    int ctas;
+    int threads;
+    int chunks;          /* (CTA, level) work units                             */
+    long long nnz;       /* stored entries incl. diagonal (nnz_T)               */
+    long long device_bytes;
+    double alg_bytes;    /* 12 nnz_T + 20 n                   */
+    double predicted_us; /* cost-model critical path of one solve               */
+} hec_tri_info;
+
+typedef struct hec_tri* hec_tri_t;
+
+/*
+ * Upload a prepared triangle. The arguments are the fields of the reference's
+ * hec::PreparedTriangular (proj/include/hecsolve/triangular.hpp:18-24):
+ * n, reversal_applied, schedule.{nlev, level_starts[nlev+1], inv_perm[n]},
+ * hec.ell.{width, col_indices[width*n], values[width*n]} (column-major),
+ * hec.csr.{row_offsets[n+1], col_indices, values} (diagonal last per row).
+ * Replaces the data the reference reads in solve() (proj/src/triangular.cpp:96-103).
+ */
+int hec_tri_create(int n, int reversal_applied, int nlev, const int* level_starts,
+                   const int* inv_perm, int ell_width, const int* ell_cols,
+                   const double* ell_vals, const int* csr_row_offsets, const int* csr_cols,
+                   const double* csr_vals, const hec_tri_options* options, hec_tri_t* out);
+
+/*
+ * x = T^-1 b in the original ordering, device pointers, enqueued on `stream`
+ * (cudaStream_t; NULL = legacy default stream). Bitwise equal to the
+ * reference's hec::solve (proj/src/triangular.cpp:90-135) for any worker count.
+ * b and x must not alias. Concurrent solves on different streams are allowed.
+ */
+int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream);
+
+/* Same with host vectors (H2D, solve, D2H; synchronous). Drop-in for hec::solve. */
+int hec_tri_solve_host(hec_tri_t t, const double* b, double* x);
+
+int hec_tri_query(hec_tri_t t, hec_tri_info* info);
+int hec_tri_destroy(hec_tri_t t);
+
+/*
+ * L+U pair with optional RAS gather/scatter: x = scatter(U^-1 L^-1 gather(r)).
+ * n_ext rows of the concatenated block ordering; gather[k] = global row feeding
+ * concatenated row k; owned[k] != 0 where part(k) owns that row (restriction).
+ * gather == NULL means the identity (n_ext == n, every row owned).
+ * The L and U arguments are the prepared fields as in hec_tri_create.
+ * Replaces hec::apply (proj/src/precond.cpp:119-145).
+ */
+typedef struct hec_precond* hec_precond_t;
+int hec_precond_create(int n, int n_ext, const int* gather, const char* owned,
+                       /* L */ int l_nlev, const int* l_level_starts, const int* l_inv_perm,
+                       int l_ell_width, const int* l_ell_cols, const double* l_ell_vals,
+                       const int* l_csr_row_offsets, const int* l_csr_cols,
+                       const double* l_csr_vals,
+                       /* U (reversal applied) */ int u_nlev, const int* u_level_starts,
+                       const int* u_inv_perm, int u_ell_width, const int* u_ell_cols,
+                       const double* u_ell_vals, const int* u_csr_row_offsets,
+                       const int* u_csr_cols, const double* u_csr_vals,
+                       const hec_tri_options* options, hec_precond_t* out);
+int hec_precond_apply(hec_precond_t m, const double* r_dev, double* x_dev, void* stream);
+int hec_precond_apply_host(hec_precond_t m, const double* r, double* x);
+int hec_precond_query(hec_precond_t m, hec_tri_info* l_info, hec_tri_info* u_info);
+int hec_precond_destroy(hec_precond_t m);
+
+/* CSR SpMV on the device: y = A x, row sums in ascending column order
+ * (bitwise equal to spmv_csr, proj/src/csr.cpp:43-57). */
+typedef struct hec_spmv* hec_spmv_t;
+int hec_spmv_create(int n_rows, int n_cols, const int* row_offsets, const int* cols,
+                    const double* vals, hec_spmv_t* out);
+int hec_spmv_run(hec_spmv_t a, const double* x_dev, double* y_dev, void* stream);
+int hec_spmv_run_host(hec_spmv_t a, const double* x, double* y);
+int hec_spmv_destroy(hec_spmv_t a);
+
+/* Restarted right-preconditioned GMRES(m) on the device (proj/src/gmres.cpp:28-137).
+ * m may be NULL. x (host, n) receives the solution. inner_residuals (host) may be
+ * NULL; otherwise it receives up to inner_capacity estimates. */
+typedef struct {
+    int restart;
+    int max_iters;
+    double rel_tol;
+    double abs_tol;
+} hec_gmres_config;
+
+typedef struct {
+    int converged;
+    int iterations;
+    double final_relative_residual;
+    double solve_seconds;
+    int n_inner;
+} hec_gmres_report;
+
+int hec_gmres_solve(hec_spmv_t a, hec_precond_t m, const double* b, const hec_gmres_config* cfg,
+                    double* x, hec_gmres_report* report, double* inner_residuals,
+                    int inner_capacity);
+
+/* ===================== Section 2: host setup ============================= */
+
+typedef struct hec_csr* hec_csr_t;   /* owns a hec::CsrMatrix */
+
+int hec_csr_create(int n_rows, int n_cols, const int* row_offsets, const int* cols,
+                   const double* vals, hec_csr_t* out);
+int hec_csr_from_triples(int n_rows, int n_cols, long long count, const int* rows,
+                         const int* cols, const double* vals, hec_csr_t* out);
+/* Borrowed views, valid until hec_csr_destroy. */
+int hec_csr_view(hec_csr_t a, int* n_rows, int* n_cols, long long* nnz,
+                 const int** row_offsets, const int** cols, const double** vals);
+int hec_csr_destroy(hec_csr_t a);
+int hec_csr_spmv_host(hec_csr_t a, const double* x, double* y, int workers);
+
+int hec_gen_poisson7(int nx, int ny, int nz, hec_csr_t* out);
+int hec_gen_poisson27(int nx, int ny, int nz, hec_csr_t* out);
+int hec_gen_reservoir7(int nx, int ny, int nz, double sigma, double kz_ratio, uint64_t seed,
+                       hec_csr_t* out);
+int hec_permute_symmetric(hec_csr_t a, const int* perm, hec_csr_t* out);
+int hec_random_ordering(int n, uint64_t seed, int* perm);
+int hec_rcm_ordering(hec_csr_t a, int* perm);
+
+int hec_ilu0(hec_csr_t a, hec_csr_t* l, hec_csr_t* u);
+int hec_ilu_k(hec_csr_t a, int k, hec_csr_t* l, hec_csr_t* u);
+int hec_ilut(hec_csr_t a, int p, double tol, hec_csr_t* l, hec_csr_t* u);
+
+/* hec::PreparedTriangular. width_mode: 0 automatic, 1 fixed(width). */
+typedef struct hec_prep* hec_prep_t;
+int hec_prepare(hec_csr_t t, int upper, int width_mode, int width, hec_prep_t* out);
+typedef struct {
+    int kind;            /* 0 lower, 1 upper */
+    int n;
+    int reversal_applied;
+    int nlev;
+    const int* level_of;
+    const int* perm;
+    const int* inv_perm;
+    const int* level_starts;
+    int ell_width;
+    const int* ell_cols;
+    const double* ell_vals;
+    const int* csr_row_offsets;
+    const int* csr_cols;
+    const double* csr_vals;
+    long long csr_nnz;
+} hec_prep_view;
+int hec_prep_view_get(hec_prep_t p, hec_prep_view* v);
+/* hec::solve on the prepared object (device mirror cached inside it). */
+int hec_prep_solve_host(hec_prep_t p, const double* b, double* x);
+/* the device triangle backing p (owned by p; do not destroy) */
+int hec_prep_device(hec_prep_t p, hec_tri_t* t);
+int hec_serial_solve(hec_csr_t t, int upper, const double* b, double* x);
+int hec_prep_destroy(hec_prep_t p);
+
+/* hec::BlockPreconditioner. kind: 0 bilu0, 1 bilut, 2 ras, 3 biluk. */
+typedef struct hec_bp* hec_bp_t;
+int hec_bp_build(hec_csr_t a, int kind, int blocks, int overlap, int ilut_p, double ilut_tol,
+                 int width_mode, int width, int fill_level, hec_bp_t* out);
+int hec_bp_dims(hec_bp_t m, int* n, int* n_parts, int* n_ext);
+/* part_of[n], offsets[n_parts+1], ext_rows[n_ext] (concatenated), owned[n_ext] */
+int hec_bp_maps(hec_bp_t m, int* part_of, int* offsets, int* ext_rows, char* owned);
+int hec_bp_prepared(hec_bp_t m, hec_prep_t* l, hec_prep_t* u); /* borrowed */
+int hec_bp_apply_host(hec_bp_t m, const double* r, double* x);
+int hec_bp_device(hec_bp_t m, hec_precond_t* d); /* borrowed */
+int hec_bp_destroy(hec_bp_t m);
+
+/* hec::gmres through the C++ drop-in (device inside). m may be NULL. */
+int hec_gmres_host(hec_csr_t a, const double* b, hec_bp_t m, const hec_gmres_config* cfg,
+                   double* x, hec_gmres_report* report, double* inner_residuals,
+                   int inner_capacity);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HECSOLVE_C_H */

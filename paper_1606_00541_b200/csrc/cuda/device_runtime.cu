@@ -1,0 +1,329 @@
+// Device runtime: construction of the B200 layouts, per-stream workspaces and
+// launches for DeviceTri / DevicePrecond / DeviceSpmv.
+
+#include "device_runtime.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "tri_kernels.cuh"
+
+namespace hec::dev {
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                             ") at " + file + ":" + std::to_string(line) + ": " + what);
+}
+
+void require_device() {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw std::runtime_error(
+            "hecsolve-b200: no CUDA device available (the B200 path has no CPU fallback)");
+    }
+}
+
+namespace {
+
+int sm_count() {
+    int dev = 0, sms = 0;
+    HEC_CUDA(cudaGetDevice(&dev));
+    HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+
+int smem_optin() {
+    int dev = 0, v = 0;
+    HEC_CUDA(cudaGetDevice(&dev));
+    HEC_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    return v;
+}
+
+inline int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+// ------------------------------------------------------------ DeviceTri ----
+DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
+    require_device();
+    plan::validate(src);
+    n_ = src.n;
+    has_out_ = src.out_map != nullptr;
+    stats_.n = src.n;
+    stats_.nlev = src.nlev;
+    long long nnz = 0;
+    if (src.n > 0) nnz = src.csr_rp[src.n];
+    for (long long k = 0; k < static_cast<long long>(src.ell_width) * src.n; ++k)
+        if (src.ell_cols[k] != static_cast<int>(k % src.n)) ++nnz;
+    stats_.nnz = nnz;
+    stats_.alg_bytes = 12.0 * static_cast<double>(nnz) + 20.0 * src.n;
+
+    strategy_ = opt.strategy == 1 ? 1 : 2;
+    if (strategy_ == 2 && n_ > 0) {
+        plan::PipelineConfig cfg;
+        cfg.ctas = opt.ctas > 0 ? opt.ctas : sm_count();
+        plan::PipelineLayout P = plan::build_pipeline(src, cfg);
+        const int budget = smem_optin() - 1024;  // static shared + slack
+        p_threads_ = opt.threads > 0 ? (opt.threads >= 256 ? 256 : 128) : (P.max_rows > 160 ? 256 : 128);
+        p_b_bytes_ = rup(8 * rup(std::max(P.max_rows, 1), 4), 128);
+        p_slot_bytes_ = p_b_bytes_ + rup(P.max_blob, 128);
+        p_ring_ = P.ring;
+        int ns = 0;
+        for (int k = 32; k >= 2; --k) {
+            const int ring_off = rup(40 * k, 16);
+            const int slot_off = rup(ring_off + 8 * (p_ring_ + 1), 128);
+            if (slot_off + k * p_slot_bytes_ <= budget) {
+                ns = k;
+                p_ring_off_ = ring_off;
+                p_slot_off_ = slot_off;
+                break;
+            }
+        }
+        if (ns >= 2) {
+            p_nslots_ = ns;
+            p_lag_ = std::max(1, ns / 2);
+            p_smem_ = p_slot_off_ + ns * p_slot_bytes_;
+            p_ctas_ = P.ctas;
+            p_kernel_ = pipeline_kernel(p_threads_);
+            HEC_CUDA(cudaFuncSetAttribute(p_kernel_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
+            p_blob_.upload(P.blob);
+            p_spans_.upload(P.span);
+            p_cta0_.upload(P.cta_chunk0);
+            stats_.ctas = p_ctas_;
+            stats_.threads = p_threads_;
+            stats_.chunks = P.chunks;
+            stats_.slots = ns;
+            stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size());
+        } else {
+            strategy_ = 1;  // a chunk too large for shared memory: level launches
+        }
+    }
+    if (strategy_ == 1 && n_ > 0) {
+        plan::LevelLayout L = plan::build_levels(src);
+        level_starts_ = L.level_starts;
+        l_width_ = L.width;
+        l_ld_ = L.ld;
+        l_bidx_.upload(L.bidx);
+        l_xidx_.upload(L.xidx);
+        if (has_out_) l_oidx_.upload(L.oidx);
+        l_ell_dep_.upload(L.ell_dep);
+        l_ell_val_.upload(L.ell_val);
+        l_diag_.upload(L.diag);
+        l_tail_rp_.upload(L.tail_rp);
+        l_tail_dep_.upload(L.tail_dep);
+        l_tail_val_.upload(L.tail_val);
+        stats_.device_bytes = static_cast<long long>(
+            4 * (L.bidx.size() + L.xidx.size() + L.oidx.size() + L.ell_dep.size() + L.tail_rp.size() +
+                 L.tail_dep.size()) +
+            8 * (L.ell_val.size() + L.diag.size() + L.tail_val.size()));
+        stats_.threads = 256;
+    }
+    stats_.strategy = strategy_;
+}
+
+DeviceTri::~DeviceTri() {
+    if (h_stream_) cudaStreamDestroy(h_stream_);
+}
+
+int DeviceTri::launches_per_solve() const {
+    if (n_ == 0) return 0;
+    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 1;
+}
+
+DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto& w = ws_[st];
+    if (!w) {
+        w = std::make_unique<Workspace>();
+        w->progress.alloc(std::max(p_ctas_, 1));
+        w->counters.alloc(2);
+        HEC_CUDA(cudaMemset(w->progress.p, 0, sizeof(uint32_t) * w->progress.count));
+        HEC_CUDA(cudaMemset(w->counters.p, 0, sizeof(uint32_t) * 2));
+    }
+    return *w;
+}
+
+void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st) {
+    if (n_ == 0) return;
+    if (strategy_ == 1) {
+        LevelArgs a{};
+        a.b = b;
+        a.xs = xs;
+        a.out = has_out_ ? out : nullptr;
+        a.bidx = l_bidx_.p;
+        a.xidx = l_xidx_.p;
+        a.oidx = l_oidx_.p;
+        a.ell_dep = l_ell_dep_.p;
+        a.ell_val = l_ell_val_.p;
+        a.diag = l_diag_.p;
+        a.tail_rp = l_tail_rp_.p;
+        a.tail_dep = l_tail_dep_.p;
+        a.tail_val = l_tail_val_.p;
+        a.width = l_width_;
+        a.ld = l_ld_;
+        launch_levels(a, level_starts_.data(), static_cast<int>(level_starts_.size()) - 1, st);
+        HEC_CUDA(cudaGetLastError());
+        return;
+    }
+    Workspace& w = workspace(st);
+    PipeArgs a{};
+    a.blobs = p_blob_.p;
+    a.spans = reinterpret_cast<const int2*>(p_spans_.p);
+    a.cta_chunk0 = p_cta0_.p;
+    a.b = b;
+    a.xs = xs;
+    a.out = has_out_ ? out : nullptr;
+    a.progress = w.progress.p;
+    a.counters = w.counters.p;
+    a.ctas = p_ctas_;
+    a.nslots = p_nslots_;
+    a.lag = p_lag_;
+    a.slot_bytes = p_slot_bytes_;
+    a.b_bytes = p_b_bytes_;
+    a.ring = p_ring_;
+    a.ring_off = p_ring_off_;
+    a.slot_off = p_slot_off_;
+    void* args[] = {&a};
+    HEC_CUDA(cudaLaunchKernel(p_kernel_, dim3(p_ctas_), dim3(96 + p_threads_), args, p_smem_, st));
+}
+
+void DeviceTri::solve_host(const double* b, double* x) {
+    if (n_ == 0) return;
+    std::lock_guard<std::mutex> g(h_mu_);  // serialises host-path callers of this handle
+    if (!h_stream_) HEC_CUDA(cudaStreamCreateWithFlags(&h_stream_, cudaStreamNonBlocking));
+    if (h_b_.count < static_cast<std::size_t>(n_)) {
+        h_b_.alloc(n_);
+        h_x_.alloc(n_);
+    }
+    const std::size_t bytes = sizeof(double) * n_;
+    HEC_CUDA(cudaMemcpyAsync(h_b_.p, b, bytes, cudaMemcpyHostToDevice, h_stream_));
+    solve(h_b_.p, h_x_.p, nullptr, h_stream_);
+    HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, bytes, cudaMemcpyDeviceToHost, h_stream_));
+    HEC_CUDA(cudaStreamSynchronize(h_stream_));
+}
+
+// -------------------------------------------------------- DevicePrecond ----
+DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
+                             plan::TriSource u, const TriOptions& opt)
+    : n_(n), n_ext_(n_ext) {
+    require_device();
+    identity_ = gather == nullptr;
+    if (identity_ && n_ext != n) throw std::invalid_argument("hec_precond_create: identity map needs n_ext == n");
+    if (l.n != n_ext || u.n != n_ext) throw std::invalid_argument("hec_precond_create: factor size mismatch");
+    std::vector<int> out_map;
+    if (!identity_) {
+        for (int k = 0; k < n_ext; ++k)
+            if (gather[k] < 0 || gather[k] >= n) throw std::invalid_argument("hec_precond_create: gather out of range");
+        out_map.resize(n_ext);
+        std::vector<int> hits(n, 0);
+        for (int k = 0; k < n_ext; ++k) {
+            out_map[k] = owned[k] ? gather[k] : -1;
+            if (owned[k]) ++hits[gather[k]];
+        }
+        for (int g = 0; g < n; ++g)
+            if (hits[g] != 1) throw std::invalid_argument("hec_precond_create: every row must be owned exactly once");
+        l.b_map = gather;           // L reads r[gather[o]]
+        u.out_map = out_map.data(); // U scatters owned rows into x
+    }
+    l_ = std::make_unique<DeviceTri>(l, opt);
+    u_ = std::make_unique<DeviceTri>(u, opt);
+}
+
+DevicePrecond::~DevicePrecond() {
+    if (h_stream_) cudaStreamDestroy(h_stream_);
+}
+
+DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto& w = ws_[st];
+    if (!w) {
+        w = std::make_unique<Workspace>();
+        w->y.alloc(std::max(n_ext_, 1));
+        if (!identity_) w->z.alloc(std::max(n_ext_, 1));
+    }
+    return *w;
+}
+
+void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
+    if (n_ == 0) return;
+    Workspace& w = workspace(st);
+    l_->solve(r, w.y.p, nullptr, st);
+    if (identity_)
+        u_->solve(w.y.p, x, nullptr, st);
+    else
+        u_->solve(w.y.p, w.z.p, x, st);
+}
+
+void DevicePrecond::apply_host(const double* r, double* x) {
+    if (n_ == 0) return;
+    std::lock_guard<std::mutex> g(h_mu_);
+    if (!h_stream_) HEC_CUDA(cudaStreamCreateWithFlags(&h_stream_, cudaStreamNonBlocking));
+    if (h_r_.count < static_cast<std::size_t>(n_)) {
+        h_r_.alloc(n_);
+        h_x_.alloc(n_);
+    }
+    const std::size_t bytes = sizeof(double) * n_;
+    HEC_CUDA(cudaMemcpyAsync(h_r_.p, r, bytes, cudaMemcpyHostToDevice, h_stream_));
+    apply(h_r_.p, h_x_.p, h_stream_);
+    HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, bytes, cudaMemcpyDeviceToHost, h_stream_));
+    HEC_CUDA(cudaStreamSynchronize(h_stream_));
+}
+
+// ----------------------------------------------------------- DeviceSpmv ----
+// Thread per row, ascending-column accumulation with separately rounded
+// multiply and add: bitwise equal to the reference's spmv_csr
+// (proj/src/csr.cpp:49-55).
+__global__ void k_spmv_csr(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* x, double* y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
+    y[i] = s;
+}
+
+// y = b - A x with A x accumulated exactly as above, then one subtraction
+// (reference residual(), proj/src/gmres.cpp:19-24).
+__global__ void k_residual_csr(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                               const double* __restrict__ v, const double* b, const double* x, double* y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
+    y[i] = __dsub_rn(b[i], s);
+}
+
+DeviceSpmv::DeviceSpmv(int n_rows, int n_cols, const int* rp, const int* ci, const double* v)
+    : n_rows_(n_rows), n_cols_(n_cols) {
+    require_device();
+    if (n_rows < 0 || n_cols < 0) throw std::invalid_argument("hec_spmv_create: negative dimension");
+    nnz_ = n_rows > 0 ? rp[n_rows] : 0;
+    rp_.upload(rp, static_cast<std::size_t>(n_rows) + 1);
+    ci_.upload(ci, static_cast<std::size_t>(nnz_));
+    v_.upload(v, static_cast<std::size_t>(nnz_));
+}
+
+void DeviceSpmv::run(const double* x, double* y, cudaStream_t st) const {
+    if (n_rows_ == 0) return;
+    k_spmv_csr<<<(n_rows_ + 255) / 256, 256, 0, st>>>(n_rows_, rp_.p, ci_.p, v_.p, x, y);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void DeviceSpmv::residual(const double* b, const double* x, double* y, cudaStream_t st) const {
+    if (n_rows_ == 0) return;
+    k_residual_csr<<<(n_rows_ + 255) / 256, 256, 0, st>>>(n_rows_, rp_.p, ci_.p, v_.p, b, x, y);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void DeviceSpmv::run_host(const double* x, double* y) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (h_x_.count < static_cast<std::size_t>(std::max(n_cols_, 1))) h_x_.alloc(std::max(n_cols_, 1));
+    if (h_y_.count < static_cast<std::size_t>(std::max(n_rows_, 1))) h_y_.alloc(std::max(n_rows_, 1));
+    HEC_CUDA(cudaMemcpy(h_x_.p, x, sizeof(double) * n_cols_, cudaMemcpyHostToDevice));
+    run(h_x_.p, h_y_.p, nullptr);
+    HEC_CUDA(cudaMemcpy(y, h_y_.p, sizeof(double) * n_rows_, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace hec::dev

@@ -1,0 +1,167 @@
+#pragma once
+// Device-side objects behind the C-ABI handles: a prepared triangle (DeviceTri),
+// an L+U preconditioner with optional RAS gather/scatter (DevicePrecond) and a
+// CSR operator (DeviceSpmv). All are immutable after construction and safe for
+// concurrent use from several streams (per-stream workspaces).
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tri_plan.hpp"
+
+namespace hec::dev {
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define HEC_CUDA(x)                                                   \
+    do {                                                              \
+        cudaError_t e_ = (x);                                         \
+        if (e_ != cudaSuccess) ::hec::dev::cuda_fail(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+// Throws std::runtime_error unless a CUDA device is usable.
+void require_device();
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    std::size_t count = 0;
+    DevBuf() = default;
+    explicit DevBuf(std::size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count) { o.p = nullptr; o.count = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; count = o.count; o.p = nullptr; o.count = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(std::size_t n) {
+        release();
+        count = n;
+        if (n) HEC_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(T)));
+    }
+    void upload(const T* src, std::size_t n) {
+        alloc(n);
+        if (n) HEC_CUDA(cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        count = 0;
+    }
+};
+
+struct TriOptions {
+    int strategy = 0;  // 0 auto, 1 levels, 2 pipeline
+    int ctas = 0;      // 0 = number of SMs
+    int threads = 0;   // solver threads per CTA (128 | 256), 0 = auto
+};
+
+struct TriStats {
+    int n = 0, nlev = 0, strategy = 0, ctas = 0, threads = 0, chunks = 0, slots = 0;
+    long long nnz = 0, device_bytes = 0;
+    double alg_bytes = 0.0, predicted_us = 0.0;
+};
+
+class DeviceTri {
+public:
+    DeviceTri(const plan::TriSource& src, const TriOptions& opt);
+    ~DeviceTri();
+    DeviceTri(const DeviceTri&) = delete;
+    DeviceTri& operator=(const DeviceTri&) = delete;
+
+    // xs[o] = solution; out[oidx] = solution where oidx >= 0 (if out != null).
+    void solve(const double* b, double* xs, double* out, cudaStream_t st);
+    // Synchronous host-vector convenience (pinned or pageable).
+    void solve_host(const double* b, double* x);
+    const TriStats& stats() const { return stats_; }
+    int n() const { return n_; }
+    int launches_per_solve() const;
+
+private:
+    struct Workspace {
+        DevBuf<uint32_t> progress, counters;
+    };
+    Workspace& workspace(cudaStream_t st);
+
+    int n_ = 0;
+    int strategy_ = 2;
+    TriStats stats_;
+    // LEVELS
+    std::vector<int> level_starts_;
+    DevBuf<int> l_bidx_, l_xidx_, l_oidx_, l_ell_dep_, l_tail_rp_, l_tail_dep_;
+    DevBuf<double> l_ell_val_, l_diag_, l_tail_val_;
+    int l_width_ = 0, l_ld_ = 0;
+    bool has_out_ = false;
+    // PIPELINE
+    DevBuf<unsigned char> p_blob_;
+    DevBuf<int> p_spans_, p_cta0_;
+    int p_ctas_ = 0, p_nslots_ = 0, p_lag_ = 0, p_slot_bytes_ = 0, p_b_bytes_ = 0;
+    int p_ring_ = 0, p_ring_off_ = 0, p_slot_off_ = 0, p_smem_ = 0, p_threads_ = 0;
+    void* p_kernel_ = nullptr;
+
+    std::mutex mu_;
+    std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
+    // host-call staging
+    std::mutex h_mu_;
+    DevBuf<double> h_b_, h_x_;
+    cudaStream_t h_stream_ = nullptr;
+};
+
+class DevicePrecond {
+public:
+    // l/u sources carry no maps; they are attached here from gather/owned.
+    DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
+                  plan::TriSource u, const TriOptions& opt);
+    void apply(const double* r, double* x, cudaStream_t st);
+    void apply_host(const double* r, double* x);
+    const DeviceTri& lower() const { return *l_; }
+    const DeviceTri& upper() const { return *u_; }
+    int n() const { return n_; }
+
+private:
+    struct Workspace {
+        DevBuf<double> y, z;
+    };
+    int n_ = 0, n_ext_ = 0;
+    bool identity_ = true;
+    std::unique_ptr<DeviceTri> l_, u_;
+    std::mutex mu_;
+    std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
+    std::mutex h_mu_;
+    DevBuf<double> h_r_, h_x_;
+    cudaStream_t h_stream_ = nullptr;
+    Workspace& workspace(cudaStream_t st);
+
+public:
+    ~DevicePrecond();
+};
+
+class DeviceSpmv {
+public:
+    DeviceSpmv(int n_rows, int n_cols, const int* rp, const int* ci, const double* v);
+    void run(const double* x, double* y, cudaStream_t st) const;
+    // y = b - A x (fused residual)
+    void residual(const double* b, const double* x, double* y, cudaStream_t st) const;
+    void run_host(const double* x, double* y);
+    int n_rows() const { return n_rows_; }
+    int n_cols() const { return n_cols_; }
+    long long nnz() const { return nnz_; }
+
+private:
+    int n_rows_ = 0, n_cols_ = 0;
+    long long nnz_ = 0;
+    DevBuf<int> rp_, ci_;
+    DevBuf<double> v_;
+    std::mutex mu_;
+    DevBuf<double> h_x_, h_y_;
+};
+
+}  // namespace hec::dev

@@ -1,0 +1,161 @@
+"""GPU parity of the triangular solve (the hot path) against the oracle.
+
+Bar: bitwise equality with the reference's Algorithm 2 (reference
+triangular.cpp:90-135) as restated in oracle/hec_oracle.c, for both device
+strategies; <= 1e-12 relative to serial substitution (the reference's own
+tolerance, test_triangular.cpp:232-254). All calls go through the C-ABI.
+"""
+import numpy as np
+import pytest
+
+from util import bits_equal, random_triangular, rel_inf_error, to_oracle, to_product
+
+pytestmark = pytest.mark.gpu
+
+STRATS = [1, 2]  # HEC_STRATEGY_LEVELS, HEC_STRATEGY_PIPELINE
+
+
+def device_solve(H, p, b, strategy, ctas=0):
+    t = H.DeviceTri.create(p, strategy=strategy, ctas=ctas)
+    return t.solve_host(b), t.info()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_hand_systems(H, strategy):
+    # reference test_triangular.cpp:150-173
+    l3 = H.csr_from_triples(3, 3, [(0, 0, 2.0), (1, 0, 1.0), (1, 1, 3.0), (2, 1, 2.0), (2, 2, 4.0)])
+    x, _ = device_solve(H, H.prepare_lower(l3), np.array([2.0, 4.0, 6.0]), strategy)
+    assert x.tolist() == [1.0, 1.0, 1.0]
+    u2 = H.csr_from_triples(2, 2, [(0, 0, 2.0), (0, 1, 1.0), (1, 1, 4.0)])
+    x, _ = device_solve(H, H.prepare_upper(u2), np.array([3.0, 4.0]), strategy)
+    assert x.tolist() == [1.0, 1.0]
+    eye = H.csr_from_triples(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0)])
+    b = np.array([5.0, -2.0, 0.5])
+    for prep in (H.prepare_lower, H.prepare_upper):
+        x, _ = device_solve(H, prep(eye), b, strategy)
+        assert bits_equal(x, b)
+
+
+def test_dropin_solve_api(H):
+    l3 = H.csr_from_triples(3, 3, [(0, 0, 2.0), (1, 0, 1.0), (1, 1, 3.0), (2, 1, 2.0), (2, 2, 4.0)])
+    p = H.prepare_lower(l3)
+    assert H.solve(p, [2.0, 4.0, 6.0]).tolist() == [1.0, 1.0, 1.0]
+    with pytest.raises(ValueError):
+        H.solve(p, [1.0, 2.0])
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("upper", [False, True])
+def test_random_systems_bitwise(H, orc, strategy, upper):
+    rng = np.random.default_rng(101 if not upper else 103)
+    for rep in range(25):
+        n = int(rng.integers(1, 400))
+        dens = float(rng.uniform(0.005, 0.3))
+        t = random_triangular(n, dens, rng, upper=upper)
+        b = rng.uniform(-1, 1, n)
+        p = (H.prepare_upper if upper else H.prepare_lower)(to_product(H, t))
+        want = orc.solve(orc.prepare(t, upper=upper), b)
+        got, _ = device_solve(H, p, b, strategy, ctas=int(rng.integers(1, 9)) if strategy == 2 else 0)
+        assert bits_equal(got, want), (rep, n)
+        serial = orc.backward(t, b) if upper else orc.forward(t, b)
+        assert rel_inf_error(got, serial) <= 1e-12
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_width_policy_invariance(H, strategy):
+    # reference test_triangular.cpp:271-281: ELL width never changes the result
+    rng = np.random.default_rng(109)
+    t = to_product(H, random_triangular(300, 0.1, rng))
+    b = rng.uniform(-1, 1, 300)
+    base, _ = device_solve(H, H.prepare_lower(t, H.WidthPolicy.fixed(0)), b, strategy)
+    for pol in (None, H.WidthPolicy.fixed(2), H.WidthPolicy.fixed(64)):
+        x, _ = device_solve(H, H.prepare_lower(t, pol), b, strategy)
+        assert bits_equal(x, base)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("gen,dims", [("gen_poisson7", (24, 20, 16)), ("gen_poisson27", (16, 14, 12)),
+                                       ("gen_reservoir7", (20, 18, 16))])
+def test_ilu0_factors_bitwise(H, orc, strategy, gen, dims):
+    a = getattr(H, gen)(*dims)
+    f = H.ilu0(a)
+    rng = np.random.default_rng(7)
+    b = rng.uniform(-1, 1, a.n_rows)
+    for fac, upper in ((f.l, False), (f.u, True)):
+        p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+        want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+        got, info = device_solve(H, p, b, strategy)
+        assert bits_equal(got, want)
+        assert info["strategy"] == strategy
+
+
+@pytest.mark.parametrize("ctas", [1, 3, 37, 148, 296])
+def test_pipeline_cta_counts(H, orc, ctas):
+    a = H.gen_poisson7(18, 17, 16)
+    f = H.ilu_k(a, 1)
+    b = np.random.default_rng(3).uniform(-1, 1, a.n_rows)
+    for fac, upper in ((f.l, False), (f.u, True)):
+        p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+        want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+        got, info = device_solve(H, p, b, 2, ctas=ctas)
+        assert bits_equal(got, want)
+
+
+def test_ilut_long_rows(H, orc):
+    # ILUT(p=40) rows exceed the sliced width cap (32) -> tail section
+    a = H.gen_reservoir7(12, 12, 10)
+    f = H.ilut(a, 40, 0.0)
+    b = np.random.default_rng(5).uniform(-1, 1, a.n_rows)
+    for fac, upper in ((f.l, False), (f.u, True)):
+        p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+        want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+        for strategy in STRATS:
+            got, _ = device_solve(H, p, b, strategy)
+            assert bits_equal(got, want)
+
+
+def test_repeated_and_device_pointer_solves(H, orc):
+    torch = pytest.importorskip("torch")
+    a = H.gen_poisson7(32, 32, 32)
+    f = H.ilu0(a)
+    p = H.prepare_lower(f.l)
+    t = H.DeviceTri.create(p, strategy=2)
+    rng = np.random.default_rng(11)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for rep in range(4):
+        b = rng.uniform(-1, 1, a.n_rows)
+        want = orc.solve(orc.prepare(to_oracle(f.l)), b)
+        bd = torch.tensor(b, device="cuda")
+        x1 = torch.empty_like(bd)
+        x2 = torch.empty_like(bd)
+        torch.cuda.synchronize()
+        t.solve(bd, x1, stream=s1)   # concurrent solves on two streams
+        t.solve(bd, x2, stream=s2)
+        torch.cuda.synchronize()
+        assert bits_equal(x1.cpu().numpy(), want)
+        assert bits_equal(x2.cpu().numpy(), want)
+
+
+def test_nonfinite_propagation(H, orc):
+    # NaN / Inf in b flow through exactly as in the reference
+    a = H.gen_poisson7(8, 8, 8)
+    f = H.ilu0(a)
+    b = np.ones(a.n_rows)
+    b[5] = np.nan
+    b[100] = np.inf
+    for fac, upper in ((f.l, False), (f.u, True)):
+        p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+        want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+        for strategy in STRATS:
+            got, _ = device_solve(H, p, b, strategy)
+            assert bits_equal(got, want)
+
+
+def test_empty_and_single(H):
+    one = H.csr_from_triples(1, 1, [(0, 0, 4.0)])
+    for strategy in STRATS:
+        x, _ = device_solve(H, H.prepare_lower(one), np.array([2.0]), strategy)
+        assert x.tolist() == [0.5]
+    empty = H.CsrMatrix.from_arrays(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0))
+    p = H.prepare_lower(empty)
+    assert H.solve(p, np.zeros(0)).shape == (0,)
