@@ -311,6 +311,18 @@ int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream)
     });
 }
 
+int hec_tri_solve_traced(hec_tri_t t, const double* b_dev, double* x_dev, void* stream,
+                         unsigned long long* trace_dev, int* cta_chunk0) {
+    return guarded([&] {
+        need(t, "hec_tri_solve_traced");
+        if (cta_chunk0) {
+            const auto& v = t->impl->cta_chunk0();
+            std::copy(v.begin(), v.end(), cta_chunk0);
+        }
+        if (b_dev && x_dev) t->impl->solve(b_dev, x_dev, nullptr, static_cast<cudaStream_t>(stream), trace_dev);
+    });
+}
+
 int hec_tri_solve_host(hec_tri_t t, const double* b, double* x) {
     return guarded([&] {
         need(t, "hec_tri_solve_host");

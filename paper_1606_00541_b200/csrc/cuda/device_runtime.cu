@@ -68,11 +68,12 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         const int budget = smem_optin() - 1024;  // static shared + slack
         p_threads_ = opt.threads > 0 ? (opt.threads >= 256 ? 256 : 128) : (P.max_rows > 160 ? 256 : 128);
         p_b_bytes_ = rup(8 * rup(std::max(P.max_rows, 1), 4), 128);
-        p_slot_bytes_ = p_b_bytes_ + rup(P.max_blob, 128);
+        p_halo_bytes_ = rup(8 * std::max(P.max_halo, 1), 128);
+        p_slot_bytes_ = p_b_bytes_ + p_halo_bytes_ + rup(P.max_blob, 128);
         p_ring_ = P.ring;
         int ns = 0;
         for (int k = 32; k >= 2; --k) {
-            const int ring_off = rup(40 * k, 16);
+            const int ring_off = rup(24 * k, 16);  // 3 mbarriers per slot
             const int slot_off = rup(ring_off + 8 * (p_ring_ + 1), 128);
             if (slot_off + k * p_slot_bytes_ <= budget) {
                 ns = k;
@@ -86,11 +87,15 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_lag_ = std::max(1, ns / 2);
             p_smem_ = p_slot_off_ + ns * p_slot_bytes_;
             p_ctas_ = P.ctas;
-            p_kernel_ = pipeline_kernel(p_threads_);
+            p_kernel_ = pipeline_kernel(p_threads_, false);
+            p_kernel_trace_ = pipeline_kernel(p_threads_, true);
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
+            HEC_CUDA(cudaFuncSetAttribute(p_kernel_trace_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
+            p_mailboxes_ = P.mailboxes;
             p_blob_.upload(P.blob);
             p_spans_.upload(P.span);
             p_cta0_.upload(P.cta_chunk0);
+            p_cta0_host_ = P.cta_chunk0;
             stats_.ctas = p_ctas_;
             stats_.threads = p_threads_;
             stats_.chunks = P.chunks;
@@ -137,15 +142,16 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
     auto& w = ws_[st];
     if (!w) {
         w = std::make_unique<Workspace>();
-        w->progress.alloc(std::max(p_ctas_, 1));
         w->counters.alloc(2);
-        HEC_CUDA(cudaMemset(w->progress.p, 0, sizeof(uint32_t) * w->progress.count));
         HEC_CUDA(cudaMemset(w->counters.p, 0, sizeof(uint32_t) * 2));
+        w->mailbox.alloc(static_cast<std::size_t>(std::max<long long>(p_mailboxes_, 1)));
+        fill_mailboxes(w->mailbox.p, static_cast<long long>(w->mailbox.count), nullptr);
+        HEC_CUDA(cudaDeviceSynchronize());
     }
     return *w;
 }
 
-void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st) {
+void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st, unsigned long long* trace) {
     if (n_ == 0) return;
     if (strategy_ == 1) {
         LevelArgs a{};
@@ -175,18 +181,21 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st)
     a.b = b;
     a.xs = xs;
     a.out = has_out_ ? out : nullptr;
-    a.progress = w.progress.p;
+    a.mbox = w.mailbox.p;
     a.counters = w.counters.p;
     a.ctas = p_ctas_;
     a.nslots = p_nslots_;
     a.lag = p_lag_;
     a.slot_bytes = p_slot_bytes_;
     a.b_bytes = p_b_bytes_;
+    a.halo_bytes = p_halo_bytes_;
     a.ring = p_ring_;
     a.ring_off = p_ring_off_;
     a.slot_off = p_slot_off_;
+    a.trace = trace;
     void* args[] = {&a};
-    HEC_CUDA(cudaLaunchKernel(p_kernel_, dim3(p_ctas_), dim3(96 + p_threads_), args, p_smem_, st));
+    HEC_CUDA(cudaLaunchKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_),
+                              dim3(kPipelineRoleThreads + p_threads_), args, p_smem_, st));
 }
 
 void DeviceTri::solve_host(const double* b, double* x) {

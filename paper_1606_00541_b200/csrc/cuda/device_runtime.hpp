@@ -78,7 +78,10 @@ public:
     DeviceTri& operator=(const DeviceTri&) = delete;
 
     // xs[o] = solution; out[oidx] = solution where oidx >= 0 (if out != null).
-    void solve(const double* b, double* xs, double* out, cudaStream_t st);
+    void solve(const double* b, double* xs, double* out, cudaStream_t st,
+               unsigned long long* trace = nullptr);
+    // chunk -> CTA map of the pipeline layout (empty for LEVELS)
+    const std::vector<int>& cta_chunk0() const { return p_cta0_host_; }
     // Synchronous host-vector convenience (pinned or pageable).
     void solve_host(const double* b, double* x);
     const TriStats& stats() const { return stats_; }
@@ -87,7 +90,8 @@ public:
 
 private:
     struct Workspace {
-        DevBuf<uint32_t> progress, counters;
+        DevBuf<uint32_t> counters;            // ticket + finished CTAs
+        DevBuf<unsigned long long> mailbox;   // cross-CTA values (sentinel = empty)
     };
     Workspace& workspace(cudaStream_t st);
 
@@ -103,9 +107,12 @@ private:
     // PIPELINE
     DevBuf<unsigned char> p_blob_;
     DevBuf<int> p_spans_, p_cta0_;
-    int p_ctas_ = 0, p_nslots_ = 0, p_lag_ = 0, p_slot_bytes_ = 0, p_b_bytes_ = 0;
+    int p_ctas_ = 0, p_nslots_ = 0, p_lag_ = 0, p_slot_bytes_ = 0, p_b_bytes_ = 0, p_halo_bytes_ = 0;
     int p_ring_ = 0, p_ring_off_ = 0, p_slot_off_ = 0, p_smem_ = 0, p_threads_ = 0;
     void* p_kernel_ = nullptr;
+    void* p_kernel_trace_ = nullptr;
+    long long p_mailboxes_ = 0;
+    std::vector<int> p_cta0_host_;
 
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;

@@ -31,19 +31,23 @@ struct PipeArgs {
     const double* b;
     double* xs;
     double* out;
-    uint32_t* progress;          // per CTA: rows finished (this launch)
+    unsigned long long* mbox;    // cross-CTA mailbox words (sentinel = empty)
     uint32_t* counters;          // [0] ticket, [1] CTAs finished
     int ctas;
     int nslots;
     int lag;
     int slot_bytes;
     int b_bytes;                 // gathered-b area at the start of each slot
+    int halo_bytes;              // staged halo values after it
     int ring;                    // ring entries (power of two)
     int ring_off;                // shared-memory byte offsets
     int slot_off;
+    unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 
 void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
-void* pipeline_kernel(int nsolve);
+void* pipeline_kernel(int nsolve, bool trace);
+void fill_mailboxes(unsigned long long* p, long long n, cudaStream_t st);
+constexpr int kPipelineRoleThreads = 64;  // producer warp + waiter warp
 
 }  // namespace hec::dev

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 namespace hec::plan {
 
@@ -142,11 +143,12 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
             const int c = owner_of_i(s.inv_perm[r]);
             Chunk ch{c, k, r, 0, 0, 0};
             while (r < re && owner_of_i(s.inv_perm[r]) == c) {
-                // would this row still fit the slot budget?
                 const int w2 = std::max(ch.w, std::min(cnt[r], cfg.max_width));
                 const int t2 = ch.ntail + std::max(0, cnt[r] - cfg.max_width);
-                const int fl = (t2 > 0 ? 1 : 0) | flags_out;
-                const int bytes = blob_sections(ch.m + 1, w2, 0, t2, fl).end + 8 * round_up(ch.m + 1, 4) + 16 * 8;
+                const int fl = (t2 > 0 ? 1 : 0) | flags_out | 4;
+                // blob + gathered b + (typical) one halo value and one mailbox per row
+                const int bytes = blob_sections(ch.m + 1, w2, ch.m + 1, ch.m + 1, t2, fl).end +
+                                  16 * round_up(ch.m + 1, 4);
                 if (ch.m > 0 && bytes > cfg.slot_cap) break;
                 ch.w = w2;
                 ch.ntail = t2;
@@ -157,8 +159,8 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
         }
     }
 
-    // 2. sequence numbers and the progress value that covers each row
-    std::vector<int> owner_r(n), seq_r(n), done_r(n), chunk_pos_r(n);
+    // 2. owner, sequence number and chunk position of every reordered row
+    std::vector<int> owner_r(n), seq_r(n), chunk_pos_r(n);
     P.cta_chunk0.assign(static_cast<std::size_t>(C) + 1, 0);
     for (int c = 0; c < C; ++c) {
         P.cta_chunk0[c + 1] = P.cta_chunk0[c] + static_cast<int>(per_cta[c].size());
@@ -168,7 +170,6 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
             for (int t = 0; t < ch.m; ++t) {
                 owner_r[ch.r0 + t] = c;
                 seq_r[ch.r0 + t] = q + t;
-                done_r[ch.r0 + t] = q + ch.m;
                 chunk_pos_r[ch.r0 + t] = static_cast<int>(j);
             }
             q += ch.m;
@@ -176,45 +177,80 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
     }
     P.chunks = P.cta_chunk0[C];
 
-    // 3. emit blobs
-    P.span.assign(2 * static_cast<std::size_t>(P.chunks), 0);
-    std::vector<std::vector<unsigned char>> cta_blob(C);
-    std::vector<long long> ring_deps(C, 0), global_deps(C, 0), waits_cnt(C, 0);
-    std::vector<int> slot_max(C, 0), rows_max(C, 0);
-    std::vector<char> bad(C, 0);
+    // 3. consumer side (parallel over CTAs): dependency codes, per-chunk halo
+    //    lists and the CTA's mailboxes (one per foreign producer row).
+    struct CtaWork {
+        std::vector<std::vector<int>> dep, tdep, tptr, halo;  // per chunk
+        std::vector<std::vector<double>> val, tval;
+        std::vector<int> mb_row;        // local mailbox -> producer reordered row
+        std::vector<int> mb_last;       // local mailbox -> last chunk that reads it
+        std::vector<char> has_global;   // per chunk: some dependency read from global x
+        long long ring_deps = 0, global_deps = 0, halo_deps = 0;
+        bool bad = false;
+    };
+    std::vector<CtaWork> work(C);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int c = 0; c < C; ++c) {
-        std::vector<int> waited(C, 0);
-        std::vector<int> need(C, 0);
-        std::vector<int> touched;
-        auto& out = cta_blob[c];
+        CtaWork& W = work[c];
+        const std::size_t nchk = per_cta[c].size();
+        W.dep.resize(nchk);
+        W.val.resize(nchk);
+        W.tdep.resize(nchk);
+        W.tval.resize(nchk);
+        W.tptr.resize(nchk);
+        W.halo.resize(nchk);
+        W.has_global.assign(nchk, 0);
+        std::unordered_map<int, int> mb_of;   // producer row -> local mailbox
+        std::unordered_map<int, int> halo_of; // local mailbox -> halo slot (this chunk)
         int q0 = 0;
-        for (std::size_t j = 0; j < per_cta[c].size(); ++j) {
+        for (std::size_t j = 0; j < nchk; ++j) {
             const Chunk& ch = per_cta[c][j];
             const int q_end = q0 + ch.m;
-            // dependency encoding + cross-CTA needs
-            touched.clear();
+            const int m = ch.m, w = ch.w, mp = round_up(m, 4);
+            halo_of.clear();
+            auto& halo = W.halo[j];
             auto encode = [&](int col) -> int {
                 const int oc = owner_r[col];
                 if (oc == c) {
-                    if (chunk_pos_r[col] >= static_cast<int>(j)) bad[c] = 1;
+                    if (chunk_pos_r[col] >= static_cast<int>(j)) W.bad = true;
                     if (seq_r[col] >= q_end - cfg.ring) {
-                        ++ring_deps[c];
+                        ++W.ring_deps;
                         return -((seq_r[col] & (cfg.ring - 1)) + 1);
                     }
-                } else {
-                    if (oc > c) bad[c] = 1;
-                    if (need[oc] == 0) touched.push_back(oc);
-                    need[oc] = std::max(need[oc], done_r[col]);
+                    ++W.global_deps;
+                    W.has_global[j] = 1;
+                    return sol_index(s, col);
                 }
-                ++global_deps[c];
-                return sol_index(s, col);
+                if (oc > c) W.bad = true;
+                auto it = mb_of.find(col);
+                int mb;
+                if (it == mb_of.end()) {
+                    mb = static_cast<int>(W.mb_row.size());
+                    mb_of.emplace(col, mb);
+                    W.mb_row.push_back(col);
+                    W.mb_last.push_back(static_cast<int>(j));
+                } else {
+                    mb = it->second;
+                    W.mb_last[mb] = static_cast<int>(j);
+                }
+                auto hit = halo_of.find(mb);
+                int h;
+                if (hit == halo_of.end()) {
+                    h = static_cast<int>(halo.size());
+                    halo_of.emplace(mb, h);
+                    halo.push_back(mb);
+                } else {
+                    h = hit->second;
+                }
+                ++W.halo_deps;
+                return -(cfg.ring + 2 + h);
             };
-            const int m = ch.m, w = ch.w, mp = round_up(m, 4);
-            std::vector<int> dep(static_cast<std::size_t>(w) * mp, -(cfg.ring + 1));
-            std::vector<double> val(static_cast<std::size_t>(w) * mp, 0.0);
-            std::vector<int> tptr(round_up(mp + 1, 4), 0), tdep;
-            std::vector<double> tval;
+            auto& dep = W.dep[j];
+            auto& val = W.val[j];
+            auto& tptr = W.tptr[j];
+            dep.assign(static_cast<std::size_t>(w) * mp, -(cfg.ring + 1));
+            val.assign(static_cast<std::size_t>(w) * mp, 0.0);
+            tptr.assign(round_up(mp + 1, 4), 0);
             for (int t = 0; t < m; ++t) {
                 const int r = ch.r0 + t;
                 int e = 0;
@@ -224,34 +260,78 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
                         dep[static_cast<std::size_t>(e) * mp + t] = d;
                         val[static_cast<std::size_t>(e) * mp + t] = v;
                     } else {
-                        tdep.push_back(d);
-                        tval.push_back(v);
+                        W.tdep[j].push_back(d);
+                        W.tval[j].push_back(v);
                     }
                     ++e;
                 });
-                tptr[t + 1] = static_cast<int>(tdep.size());
+                tptr[t + 1] = static_cast<int>(W.tdep[j].size());
             }
-            for (int t = m; t < round_up(mp + 1, 4) - 1; ++t) tptr[t + 1] = tptr[t];
-            std::vector<int> waits;
-            for (int oc : touched) {
-                if (need[oc] > waited[oc]) {
-                    waits.push_back(oc);
-                    waits.push_back(need[oc]);
-                    waited[oc] = need[oc];
-                }
-                need[oc] = 0;
+            for (int t = m; t < static_cast<int>(tptr.size()) - 1; ++t) tptr[t + 1] = tptr[t];
+            q0 = q_end;
+        }
+    }
+    for (int c = 0; c < C; ++c)
+        if (work[c].bad) throw std::invalid_argument("hec_tri_create: dependency order violates the level schedule");
+
+    // 4. global mailbox ids and the producer-side lists (reordered row -> ids)
+    std::vector<long long> mb_base(static_cast<std::size_t>(C) + 1, 0);
+    for (int c = 0; c < C; ++c) mb_base[c + 1] = mb_base[c] + static_cast<long long>(work[c].mb_row.size());
+    P.mailboxes = mb_base[C];
+    if (P.mailboxes > 0x3fffffffLL) throw std::overflow_error("hec_tri_create: too many cross-CTA values");
+    std::vector<int> feed_ptr(static_cast<std::size_t>(n) + 1, 0);
+    for (int c = 0; c < C; ++c)
+        for (int r : work[c].mb_row) ++feed_ptr[r + 1];
+    for (int r = 0; r < n; ++r) feed_ptr[r + 1] += feed_ptr[r];
+    std::vector<int> feed(static_cast<std::size_t>(feed_ptr[n]));
+    {
+        std::vector<int> fill(feed_ptr.begin(), feed_ptr.end() - 1);
+        for (int c = 0; c < C; ++c)
+            for (std::size_t l = 0; l < work[c].mb_row.size(); ++l)
+                feed[fill[work[c].mb_row[l]]++] = static_cast<int>(mb_base[c] + static_cast<long long>(l));
+    }
+
+    // 5. emit blobs (parallel over CTAs)
+    P.span.assign(2 * static_cast<std::size_t>(P.chunks), 0);
+    std::vector<std::vector<unsigned char>> cta_blob(C);
+    std::vector<int> blob_max(C, 0), rows_max(C, 0), halo_max(C, 0);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < C; ++c) {
+        CtaWork& W = work[c];
+        auto& out = cta_blob[c];
+        int q0 = 0;
+        for (std::size_t j = 0; j < per_cta[c].size(); ++j) {
+            const Chunk& ch = per_cta[c][j];
+            const int m = ch.m, w = ch.w, mp = round_up(m, 4);
+            std::vector<int> mbptr(round_up(mp + 1, 4), 0), mbid;
+            for (int t = 0; t < m; ++t) {
+                const int r = ch.r0 + t;
+                for (int k = feed_ptr[r]; k < feed_ptr[r + 1]; ++k) mbid.push_back(feed[k]);
+                mbptr[t + 1] = static_cast<int>(mbid.size());
             }
-            const int nwait = static_cast<int>(waits.size() / 2);
-            waits_cnt[c] += nwait;
-            const int ntail = static_cast<int>(tdep.size());
-            const int flags = (ntail > 0 ? 1 : 0) | flags_out;
-            const BlobSections sec = blob_sections(m, w, nwait, ntail, flags);
+            for (int t = m; t < static_cast<int>(mbptr.size()) - 1; ++t) mbptr[t + 1] = mbptr[t];
+            const int nmb = static_cast<int>(mbid.size());
+            const int nhalo = static_cast<int>(W.halo[j].size());
+            const int ntail = static_cast<int>(W.tdep[j].size());
+            const int flags = (ntail > 0 ? 1 : 0) | flags_out | (nmb > 0 ? 4 : 0) | (W.has_global[j] ? 8 : 0);
+            const BlobSections sec = blob_sections(m, w, nhalo, nmb, ntail, flags);
             const std::size_t base = out.size();
             out.resize(base + sec.end, 0);
             unsigned char* b = out.data() + base;
-            const int hdr[8] = {m, w, q0, flags, nwait, ntail, 0, 0};
-            std::memcpy(b, hdr, sizeof(hdr));
-            if (nwait) std::memcpy(b + 32, waits.data(), 8 * static_cast<std::size_t>(nwait));
+            const ChunkHeader hdr{m,        w,         q0,       flags,    nhalo,    ntail,     nmb,
+                                  mp,       sec.halo,  sec.mbptr, sec.mbid, sec.diag, sec.val,   sec.dep,
+                                  sec.bidx, sec.xidx,  sec.oidx, sec.tptr, sec.tval, sec.tdep, {0, 0, 0, 0}};
+            std::memcpy(b, &hdr, sizeof(hdr));
+            for (int h = 0; h < nhalo; ++h) {
+                const int l = W.halo[j][h];
+                const long long gid = mb_base[c] + l;
+                const int code = static_cast<int>(gid * 2 + (W.mb_last[l] == static_cast<int>(j) ? 1 : 0));
+                std::memcpy(b + sec.halo + 4 * h, &code, 4);
+            }
+            if (flags & 4) {
+                std::memcpy(b + sec.mbptr, mbptr.data(), 4 * mbptr.size());
+                std::memcpy(b + sec.mbid, mbid.data(), 4 * mbid.size());
+            }
             auto put_i = [&](int off, int idx, int v) { std::memcpy(b + off + 4 * idx, &v, 4); };
             auto put_d = [&](int off, int idx, double v) { std::memcpy(b + off + 8 * idx, &v, 8); };
             for (int t = 0; t < m; ++t) {
@@ -262,29 +342,27 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
                 put_i(sec.xidx, t, o);
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
             }
-            for (int t = m; t < mp; ++t) {  // padded rows are never processed
-                put_i(sec.bidx, t, 0);
-                put_i(sec.xidx, t, 0);
-            }
-            std::memcpy(b + sec.val, val.data(), 8 * val.size());
-            std::memcpy(b + sec.dep, dep.data(), 4 * dep.size());
+            std::memcpy(b + sec.val, W.val[j].data(), 8 * W.val[j].size());
+            std::memcpy(b + sec.dep, W.dep[j].data(), 4 * W.dep[j].size());
             if (flags & 1) {
-                std::memcpy(b + sec.tptr, tptr.data(), 4 * tptr.size());
-                std::memcpy(b + sec.tval, tval.data(), 8 * tval.size());
-                std::memcpy(b + sec.tdep, tdep.data(), 4 * tdep.size());
+                std::memcpy(b + sec.tptr, W.tptr[j].data(), 4 * W.tptr[j].size());
+                std::memcpy(b + sec.tval, W.tval[j].data(), 8 * W.tval[j].size());
+                std::memcpy(b + sec.tdep, W.tdep[j].data(), 4 * W.tdep[j].size());
             }
-            slot_max[c] = std::max(slot_max[c], sec.end);
+            blob_max[c] = std::max(blob_max[c], sec.end);
             rows_max[c] = std::max(rows_max[c], m);
+            halo_max[c] = std::max(halo_max[c], nhalo);
             const int gj = P.cta_chunk0[c] + static_cast<int>(j);
             P.span[2 * gj + 0] = static_cast<int>(base / 16);  // CTA-relative for now
             P.span[2 * gj + 1] = sec.end;
-            q0 = q_end;
+            q0 += m;
+            // free the consumer-side scratch as we go
+            std::vector<int>().swap(W.dep[j]);
+            std::vector<double>().swap(W.val[j]);
         }
     }
-    for (int c = 0; c < C; ++c)
-        if (bad[c]) throw std::invalid_argument("hec_tri_create: dependency order violates the level schedule");
 
-    // 4. concatenate CTA streams (16-byte aligned offsets)
+    // 6. concatenate CTA streams (16-byte aligned offsets)
     std::size_t total = 0;
     std::vector<std::size_t> cta_base(C);
     for (int c = 0; c < C; ++c) {
@@ -295,13 +373,15 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
     P.blob.resize(total);
     for (int c = 0; c < C; ++c) {
         std::memcpy(P.blob.data() + cta_base[c], cta_blob[c].data(), cta_blob[c].size());
+        std::vector<unsigned char>().swap(cta_blob[c]);
         for (int gj = P.cta_chunk0[c]; gj < P.cta_chunk0[c + 1]; ++gj)
             P.span[2 * gj] += static_cast<int>(cta_base[c] / 16);
-        P.max_blob = std::max(P.max_blob, slot_max[c]);
+        P.max_blob = std::max(P.max_blob, blob_max[c]);
         P.max_rows = std::max(P.max_rows, rows_max[c]);
-        P.ring_deps += ring_deps[c];
-        P.global_deps += global_deps[c];
-        P.cross_waits += waits_cnt[c];
+        P.max_halo = std::max(P.max_halo, halo_max[c]);
+        P.ring_deps += work[c].ring_deps;
+        P.global_deps += work[c].global_deps;
+        P.halo_deps += work[c].halo_deps;
     }
     return P;
 }

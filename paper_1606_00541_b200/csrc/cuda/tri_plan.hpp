@@ -56,21 +56,37 @@ LevelLayout build_levels(const TriSource& s);
 // Persistent kernel, CTA c owns lower-frame rows [c*per, (c+1)*per). Its rows
 // of one level form a contiguous reordered range ("chunk"); chunks are laid out
 // back to back per CTA as self-describing 16-byte-aligned blobs that one
-// cp.async.bulk moves into shared memory. Blob layout (mp = round_up(m, 4)):
-//   int4  {m, w, q0, flags}         flags: 1 tail, 2 out-map
-//   int4  {nwait, ntail, 0, 0}
-//   int2  waits[nwait]  (cta, progress needed), padded to 16 B
+// cp.async.bulk moves into shared memory.
+//
+// Cross-CTA values travel through MAILBOXES: one FP64 word per (producer row,
+// consumer CTA) pair. The producing solver thread stores x there (plain store,
+// no fence); the consumer's waiter warp polls the word until it no longer holds
+// the sentinel (a signalling NaN, which IEEE arithmetic can never produce),
+// stages it into shared memory, and re-arms the word with the sentinel after
+// its last use in this solve. No progress counters, no release/acquire fences.
+//
+// Blob layout (mp = round_up(m, 4)):
+//   ChunkHeader (96 B: counts + every section offset, so the device decodes a
+//                chunk with six 16-byte shared loads)
+//                flags: 1 tail, 2 out-map, 4 mailbox stores, 8 global deps
+//   int   halo[nhalo]   mailbox id * 2 + (1 if last use -> re-arm), pad 16 B
+//   int   mbptr[mp+1]   (flags & 4) per-row range into mbid, pad 16 B
+//   int   mbid[nmb]     (flags & 4) mailbox ids this chunk's rows feed, pad 16 B
 //   double diag[mp]
 //   double val[w][mp]               sliced ELL, slot-major
-//   int    dep[w][mp]               >= 0 solution index (global); < 0 ring slot -(s+1)
+//   int    dep[w][mp]               >= 0 solution index (global, own rows older than the ring)
+//                                    < 0: s = -d-1; s < ring: x ring slot; s == ring: 0.0;
+//                                         s > ring: staged halo value s-ring-1
 //   int    bidx[mp], xidx[mp], (oidx[mp] if flags & 2)
 //   if flags & 1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
-// Shared-memory footprint of a chunk = blob + 8 * mp bytes (gathered b).
+// Shared-memory footprint of a chunk = blob + 8 * mp (gathered b) + 8 * nhalo.
+constexpr unsigned long long kMailboxEmpty = 0x7FF4DEADBEEF0001ULL;  // signalling NaN
+
 struct PipelineConfig {
     int ctas = 148;
     int ring = 4096;          // x ring entries (power of two); slot `ring` holds 0.0
     int max_width = 32;       // sliced-ELL width cap; longer rows spill to the tail
-    int slot_cap = 24576;     // max shared-memory bytes of one chunk
+    int slot_cap = 24576;     // target shared-memory bytes of one chunk
 };
 
 struct PipelineLayout {
@@ -78,33 +94,50 @@ struct PipelineLayout {
     int max_blob = 0;                     // bytes of the largest blob
     int chunks = 0;
     int max_rows = 0;                     // rows of the largest chunk
+    int max_halo = 0;                     // halo values of the largest chunk
     bool has_out = false;
+    long long mailboxes = 0;              // (producer row, consumer CTA) words
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
     std::vector<int> span;                // 2 per chunk: (offset / 16, bytes)
     std::vector<unsigned char> blob;      // all chunk blobs, 16-byte aligned
-    long long cross_waits = 0;            // (chunk, cta) waits after pruning
-    long long ring_deps = 0, global_deps = 0;
+    long long ring_deps = 0, global_deps = 0, halo_deps = 0;
 };
 PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg);
 
-// Blob section offsets (bytes from the blob start), shared with the kernel.
+// Blob section offsets (bytes from the blob start).
 struct BlobSections {
-    int diag, val, dep, bidx, xidx, oidx, tptr, tval, tdep, end;
+    int halo, mbptr, mbid, diag, val, dep, bidx, xidx, oidx, tptr, tval, tdep, end;
 };
+
+// First 96 bytes of every blob; read by the kernel as-is.
+struct ChunkHeader {
+    int m, w, q0, flags;
+    int nhalo, ntail, nmb, mp;
+    int halo, mbptr, mbid, diag;
+    int val, dep, bidx, xidx;
+    int oidx, tptr, tval, tdep;
+    int pad[4];
+};
+static_assert(sizeof(ChunkHeader) == 96, "chunk header is six 16-byte words");
+constexpr int kChunkHeaderBytes = 96;
+
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
-inline BlobSections blob_sections(int m, int w, int nwait, int ntail, int flags) {
+inline BlobSections blob_sections(int m, int w, int nhalo, int nmb, int ntail, int flags) {
     BlobSections b{};
     const int mp = round_up(m, 4);
-    int at = 32 + round_up(8 * nwait, 16);
-    b.diag = at; at += 8 * mp;
-    b.val = at;  at += 8 * mp * w;
-    b.dep = at;  at += 4 * mp * w;
-    b.bidx = at; at += 4 * mp;
-    b.xidx = at; at += 4 * mp;
-    b.oidx = at; if (flags & 2) at += 4 * mp;
-    b.tptr = at; if (flags & 1) at += 4 * round_up(mp + 1, 4);
-    b.tval = at; if (flags & 1) at += 8 * round_up(ntail, 2);
-    b.tdep = at; if (flags & 1) at += 4 * round_up(ntail, 4);
+    int at = kChunkHeaderBytes;
+    b.halo = at;  at += round_up(4 * nhalo, 16);
+    b.mbptr = at; if (flags & 4) at += 4 * round_up(mp + 1, 4);
+    b.mbid = at;  if (flags & 4) at += round_up(4 * nmb, 16);
+    b.diag = at;  at += 8 * mp;
+    b.val = at;   at += 8 * mp * w;
+    b.dep = at;   at += 4 * mp * w;
+    b.bidx = at;  at += 4 * mp;
+    b.xidx = at;  at += 4 * mp;
+    b.oidx = at;  if (flags & 2) at += 4 * mp;
+    b.tptr = at;  if (flags & 1) at += 4 * round_up(mp + 1, 4);
+    b.tval = at;  if (flags & 1) at += 8 * round_up(ntail, 2);
+    b.tdep = at;  if (flags & 1) at += 4 * round_up(ntail, 4);
     b.end = at;
     return b;
 }

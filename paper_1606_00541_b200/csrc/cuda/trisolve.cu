@@ -14,17 +14,21 @@
 //                   lower-frame rows; its rows of level k form one chunk. Warp
 //                   roles: 0 = producer (cp.async.bulk of the next chunk blobs
 //                   into a shared-memory slot ring + cp.async gather of b),
-//                   1 = waiter (acquire-polls the progress counters of the
-//                   CTAs a chunk depends on), 2 = publisher (release-stores this
-//                   CTA's progress), 3.. = solvers. Own recent x values live in
-//                   a shared-memory ring; older / foreign ones come from L2.
-//                   Level barriers become point-to-point CTA progress waits.
+//                   1 = waiter (polls the mailbox words carrying the foreign x
+//                   values a chunk needs and stages them in shared memory),
+//                   2.. = solvers (own recent x values from a shared-memory
+//                   ring; foreign ones from the staged halo). The reference's
+//                   level barrier becomes a per-value dataflow handoff: the
+//                   producing thread's plain 8-byte store IS the signal (the
+//                   empty sentinel is a signalling NaN no arithmetic result can
+//                   equal), so no fence or flag sits on the critical path.
 
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "tri_kernels.cuh"
+#include "tri_plan.hpp"
 
 namespace hec::dev {
 
@@ -70,16 +74,21 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 // IEEE row update, never contracted into an FMA.
@@ -116,41 +125,82 @@ void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, c
 }
 
 // ------------------------------------------------------------ PIPELINE ----
-struct ChunkHeader {
-    int m, w, q0, flags;
-    int nwait, ntail, pad0, pad1;
-};
+using plan::ChunkHeader;
+constexpr unsigned long long kEmpty = plan::kMailboxEmpty;
 
-__device__ __forceinline__ int rup(int v, int m) { return (v + m - 1) / m * m; }
-
-struct Sections {
-    int diag, val, dep, bidx, xidx, oidx, tptr, tval, tdep;
-};
-__device__ __forceinline__ Sections sections(const ChunkHeader& h) {
-    Sections s;
-    const int mp = rup(h.m, 4);
-    int at = 32 + rup(8 * h.nwait, 16);
-    s.diag = at; at += 8 * mp;
-    s.val = at;  at += 8 * mp * h.w;
-    s.dep = at;  at += 4 * mp * h.w;
-    s.bidx = at; at += 4 * mp;
-    s.xidx = at; at += 4 * mp;
-    s.oidx = at; if (h.flags & 2) at += 4 * mp;
-    s.tptr = at; if (h.flags & 1) at += 4 * rup(mp + 1, 4);
-    s.tval = at; if (h.flags & 1) at += 8 * rup(h.ntail, 2);
-    s.tdep = at;
-    return s;
+// Shared-memory word of dependency code d < 0 (see tri_plan.hpp): the own-x
+// ring, its zero slot, or -- beyond the zero slot -- the chunk's staged halo,
+// which sits `hoff` doubles further from the ring base.
+__device__ __forceinline__ int smem_word(int d, int ring_n, int hoff) {
+    const int s = -d - 1;
+    return s + (s > ring_n ? hoff : 0);
 }
 
-template <int NSOLVE>
-__global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
+// Any dependency code, including d >= 0 (own rows older than the ring: global x).
+__device__ __forceinline__ double dep_value(int d, const double* xs, const double* ring, int ring_n, int hoff) {
+    double v = ring[d < 0 ? smem_word(d, ring_n, hoff) : 0];
+    if (d >= 0) v = xs[d];
+    return v;
+}
+
+// acc -= sum over W sliced-ELL slots, all loads issued before the FP chain.
+template <int W>
+__device__ __forceinline__ double accumulate_fixed(double acc, const int* dep, const double* val, int mp, int t,
+                                                   const double* ring, int ring_n, int hoff) {
+    double xv[W], vv[W];
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+        xv[u] = ring[smem_word(dep[u * mp + t], ring_n, hoff)];
+        vv[u] = val[u * mp + t];
+    }
+#pragma unroll
+    for (int u = 0; u < W; ++u) acc = sub_prod(acc, vv[u], xv[u]);
+    return acc;
+}
+
+// Runtime width, any dependency kind (global x allowed); groups of 8 loads.
+__device__ __noinline__ double accumulate_generic(double acc, int w, const int* dep, const double* val, int mp, int t,
+                                                  const double* xs, const double* ring, int ring_n, int hoff) {
+    for (int k0 = 0; k0 < w; k0 += 8) {
+        double xv[8], vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool on = k0 + u < w;
+            const int d = on ? dep[(k0 + u) * mp + t] : -(ring_n + 1);
+            vv[u] = on ? val[(k0 + u) * mp + t] : 0.0;
+            xv[u] = dep_value(d, xs, ring, ring_n, hoff);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k0 + u < w) acc = sub_prod(acc, vv[u], xv[u]);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double accumulate(double acc, int w, bool global, const int* dep, const double* val,
+                                             int mp, int t, const double* xs, const double* ring, int ring_n,
+                                             int hoff) {
+    if (!global) {
+        switch (w) {
+#define HEC_W(N) \
+    case N: return accumulate_fixed<N>(acc, dep, val, mp, t, ring, ring_n, hoff);
+            case 0: return acc;
+            HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
+            HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
+#undef HEC_W
+            default: break;
+        }
+    }
+    return accumulate_generic(acc, w, dep, val, mp, t, xs, ring, ring_n, hoff);
+}
+
+template <int NSOLVE, bool TRACE>
+__global__ void __launch_bounds__(kPipelineRoleThreads + NSOLVE, 1) k_pipeline(PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int NS = a.nslots;
     uint64_t* bar_full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* bar_ready = bar_full + NS;
-    uint64_t* bar_clear = bar_ready + NS;
-    uint64_t* bar_done = bar_clear + NS;
-    uint64_t* bar_empty = bar_done + NS;
+    uint64_t* bar_clear = bar_full + NS;
+    uint64_t* bar_empty = bar_clear + NS;
     double* ring = reinterpret_cast<double*>(smem + a.ring_off);
     unsigned char* slots = smem + a.slot_off;
     __shared__ int s_cta;
@@ -161,9 +211,8 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
         s_cta = static_cast<int>(atomicAdd(&a.counters[0], 1u));
         for (int s = 0; s < NS; ++s) {
             mbar_init(&bar_full[s], 1);
-            mbar_init(&bar_ready[s], 32);
-            mbar_init(&bar_clear[s], 1);
-            mbar_init(&bar_done[s], 1);
+            // 32 producer lanes (b gather, cp.async arrive-on) + the waiter's arrive
+            mbar_init(&bar_clear[s], 33);
             mbar_init(&bar_empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -173,11 +222,13 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
     const int c = s_cta;
     const int c0 = a.cta_chunk0[c];
     const int nch = a.cta_chunk0[c + 1] - c0;
+    // slot = [gathered b : b_bytes][staged halo : halo_bytes][blob]
     auto slot_ptr = [&](int s) { return slots + static_cast<size_t>(s) * a.slot_bytes; };
-    // slot = [gathered b : a.b_bytes][blob]
+    const int blob_off = a.b_bytes + a.halo_bytes;
+    auto tr = [&](int j, int k) -> unsigned long long& { return a.trace[static_cast<size_t>(c0 + j) * 16 + k]; };
 
     if (warp == 0) {
-        // ---------------- producer ----------------
+        // ---------------- producer: blob prefetch + b gather ----------------
         const int lag = a.lag;
         int2 span_reg = make_int2(0, 0);
         for (int j = 0; j < nch + lag; ++j) {
@@ -191,8 +242,9 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
                 const int s = j % NS, use = j / NS;
                 if (use > 0) mbar_wait(&bar_empty[s], (use - 1) & 1);
                 if (lane == 0) {
+                    if (TRACE) tr(j, 0) = gtimer();
                     mbar_expect_tx(&bar_full[s], static_cast<uint32_t>(bytes));
-                    bulk_g2s(slot_ptr(s) + a.b_bytes, a.blobs + static_cast<size_t>(off16) * 16,
+                    bulk_g2s(slot_ptr(s) + blob_off, a.blobs + static_cast<size_t>(off16) * 16,
                              static_cast<uint32_t>(bytes), &bar_full[s]);
                 }
                 __syncwarp();
@@ -202,88 +254,110 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
                 const int s = g % NS, use = g / NS;
                 mbar_wait(&bar_full[s], use & 1);
                 unsigned char* sp = slot_ptr(s);
-                const ChunkHeader h = *reinterpret_cast<const ChunkHeader*>(sp + a.b_bytes);
-                const Sections sec = sections(h);
-                const int* bidx = reinterpret_cast<const int*>(sp + a.b_bytes + sec.bidx);
+                const ChunkHeader* h = reinterpret_cast<const ChunkHeader*>(sp + blob_off);
+                const int m = h->m;
+                const int* bidx = reinterpret_cast<const int*>(sp + blob_off + h->bidx);
                 double* bst = reinterpret_cast<double*>(sp);
-                for (int t = lane; t < h.m; t += 32) cp_async8(bst + t, a.b + bidx[t]);
-                cp_async_arrive(&bar_ready[s]);
+                if (TRACE && lane == 0) tr(g, 1) = gtimer();
+                for (int t = lane; t < m; t += 32) cp_async8(bst + t, a.b + bidx[t]);
+                cp_async_arrive(&bar_clear[s]);
             }
         }
     } else if (warp == 1) {
-        // ---------------- waiter ----------------
+        // ---------------- waiter: poll foreign values, stage them ----------------
         for (int j = 0; j < nch; ++j) {
             const int s = j % NS, use = j / NS;
             mbar_wait(&bar_full[s], use & 1);
-            mbar_wait(&bar_ready[s], use & 1);
-            const unsigned char* blob = slot_ptr(s) + a.b_bytes;
-            const ChunkHeader h = *reinterpret_cast<const ChunkHeader*>(blob);
-            const int2* waits = reinterpret_cast<const int2*>(blob + 32);
-            for (int t = lane; t < h.nwait; t += 32) {
-                const int2 wv = waits[t];
-                const uint32_t* pc = a.progress + wv.x;
-                while (ld_acquire(pc) < static_cast<uint32_t>(wv.y)) {
+            unsigned char* sp = slot_ptr(s);
+            const unsigned char* blob = sp + blob_off;
+            const int nhalo = reinterpret_cast<const ChunkHeader*>(blob)->nhalo;
+            if (TRACE && lane == 0) tr(j, 2) = gtimer();
+            const int* hcode = reinterpret_cast<const int*>(blob + plan::kChunkHeaderBytes);
+            double* hst = reinterpret_cast<double*>(sp + a.b_bytes);
+            for (int t0 = 0; t0 < nhalo; t0 += 128) {
+                unsigned long long v[4];
+                int code[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {  // 4 polls in flight per lane
+                    const int t = t0 + u * 32 + lane;
+                    code[u] = t < nhalo ? hcode[t] : -1;
+                    v[u] = code[u] >= 0 ? ld_relaxed_u64(a.mbox + (code[u] >> 1)) : 0ULL;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (code[u] < 0) continue;
+                    unsigned long long* mb = a.mbox + (code[u] >> 1);
+                    while (v[u] == kEmpty) v[u] = ld_relaxed_u64(mb);
+                    hst[t0 + u * 32 + lane] = __longlong_as_double(static_cast<long long>(v[u]));
+                    if (code[u] & 1) st_relaxed_u64(mb, kEmpty);  // last use this solve: re-arm
                 }
             }
             __syncwarp();
+            if (TRACE && lane == 0) tr(j, 3) = gtimer();
             if (lane == 0) mbar_arrive(&bar_clear[s]);
         }
-    } else if (warp == 2) {
-        // ---------------- publisher ----------------
-        if (lane == 0) {
-            for (int j = 0; j < nch; ++j) {
-                const int s = j % NS, use = j / NS;
-                mbar_wait(&bar_done[s], use & 1);
-                const ChunkHeader* h = reinterpret_cast<const ChunkHeader*>(slot_ptr(s) + a.b_bytes);
-                const uint32_t q_end = static_cast<uint32_t>(h->q0 + h->m);
-                st_release(a.progress + c, q_end);
-                mbar_arrive(&bar_empty[s]);
-            }
-        }
     } else {
-        // ---------------- solvers ----------------
-        const int st = tid - 96;
+        // ---------------- solvers: one row per thread per pass ----------------
+        const int st = tid - kPipelineRoleThreads;
         const int ring_mask = a.ring - 1;
+        const int ring_n = a.ring;
         for (int j = 0; j < nch; ++j) {
             const int s = j % NS, use = j / NS;
             mbar_wait(&bar_clear[s], use & 1);
+            long long clk0 = 0;
+            if (TRACE && st == 0) {
+                tr(j, 4) = gtimer();
+                clk0 = clock64();
+            }
             unsigned char* sp = slot_ptr(s);
-            const unsigned char* blob = sp + a.b_bytes;
+            const unsigned char* blob = sp + blob_off;
             const ChunkHeader h = *reinterpret_cast<const ChunkHeader*>(blob);
-            const Sections sec = sections(h);
-            const int mp = rup(h.m, 4);
             const double* bst = reinterpret_cast<const double*>(sp);
-            const double* diag = reinterpret_cast<const double*>(blob + sec.diag);
-            const double* val = reinterpret_cast<const double*>(blob + sec.val);
-            const int* dep = reinterpret_cast<const int*>(blob + sec.dep);
-            const int* xidx = reinterpret_cast<const int*>(blob + sec.xidx);
+            // staged halo, addressed relative to the ring base (both in shared memory)
+            const int hoff =
+                static_cast<int>((sp + a.b_bytes - reinterpret_cast<unsigned char*>(ring)) / 8) - (ring_n + 1);
+            const bool global = (h.flags & 8) != 0;
+            if (TRACE && st == 0) tr(j, 8) = clock64() - clk0;
             for (int t = st; t < h.m; t += NSOLVE) {
-                double acc = bst[t];
-                for (int k = 0; k < h.w; ++k) {
-                    const int d = dep[k * mp + t];
-                    const double xv = d >= 0 ? a.xs[d] : ring[-d - 1];
-                    acc = sub_prod(acc, val[k * mp + t], xv);
-                }
+                double acc = accumulate(bst[t], h.w, global, reinterpret_cast<const int*>(blob + h.dep),
+                                        reinterpret_cast<const double*>(blob + h.val), h.mp, t, a.xs, ring, ring_n,
+                                        hoff);
                 if (h.flags & 1) {
-                    const int* tptr = reinterpret_cast<const int*>(blob + sec.tptr);
-                    const double* tval = reinterpret_cast<const double*>(blob + sec.tval);
-                    const int* tdep = reinterpret_cast<const int*>(blob + sec.tdep);
-                    for (int e = tptr[t]; e < tptr[t + 1]; ++e) {
-                        const int d = tdep[e];
-                        const double xv = d >= 0 ? a.xs[d] : ring[-d - 1];
-                        acc = sub_prod(acc, tval[e], xv);
-                    }
+                    const int* tptr = reinterpret_cast<const int*>(blob + h.tptr);
+                    const double* tval = reinterpret_cast<const double*>(blob + h.tval);
+                    const int* tdep = reinterpret_cast<const int*>(blob + h.tdep);
+                    for (int e = tptr[t]; e < tptr[t + 1]; ++e)
+                        acc = sub_prod(acc, tval[e], dep_value(tdep[e], a.xs, ring, ring_n, hoff));
                 }
-                const double x = __ddiv_rn(acc, diag[t]);
+                if (TRACE && t == 0) {
+                    asm volatile("" ::"d"(acc) : "memory");
+                    tr(j, 9) = clock64() - clk0;
+                }
+                const double x = __ddiv_rn(acc, reinterpret_cast<const double*>(blob + h.diag)[t]);
+                if (TRACE && t == 0) {
+                    asm volatile("" ::"d"(x) : "memory");
+                    tr(j, 10) = clock64() - clk0;
+                }
+                if (h.flags & 4) {  // feed the consumers' mailboxes first: they are on the critical path
+                    const int* mbptr = reinterpret_cast<const int*>(blob + h.mbptr);
+                    const int* mbid = reinterpret_cast<const int*>(blob + h.mbid);
+                    const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
+                    for (int k = mbptr[t]; k < mbptr[t + 1]; ++k) st_relaxed_u64(a.mbox + mbid[k], xb);
+                }
                 ring[(h.q0 + t) & ring_mask] = x;
-                a.xs[xidx[t]] = x;
+                a.xs[reinterpret_cast<const int*>(blob + h.xidx)[t]] = x;
                 if (h.flags & 2) {
-                    const int o = reinterpret_cast<const int*>(blob + sec.oidx)[t];
+                    const int o = reinterpret_cast<const int*>(blob + h.oidx)[t];
                     if (o >= 0) a.out[o] = x;
                 }
             }
+            if (TRACE && st == 0) tr(j, 11) = clock64() - clk0;
             named_bar_sync(1, NSOLVE);
-            if (st == 0) mbar_arrive(&bar_done[s]);
+            if (TRACE && st == 0) {
+                tr(j, 5) = gtimer();
+                tr(j, 7) = static_cast<unsigned long long>(clock64() - clk0);
+            }
+            if (st == 0) mbar_arrive(&bar_empty[s]);
         }
     }
 
@@ -292,8 +366,7 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
         __threadfence();
         const uint32_t finished = atomicAdd(&a.counters[1], 1u);
         if (finished == static_cast<uint32_t>(a.ctas) - 1) {
-            // last CTA out: re-arm the workspace for the next launch on this stream
-            for (int k = 0; k < a.ctas; ++k) a.progress[k] = 0;
+            // last CTA out: re-arm the tickets for the next launch on this stream
             a.counters[0] = 0;
             a.counters[1] = 0;
             __threadfence();
@@ -301,11 +374,29 @@ __global__ void __launch_bounds__(96 + NSOLVE, 1) k_pipeline(PipeArgs a) {
     }
 }
 
-template __global__ void k_pipeline<128>(PipeArgs);
-template __global__ void k_pipeline<256>(PipeArgs);
+template __global__ void k_pipeline<128, false>(PipeArgs);
+template __global__ void k_pipeline<256, false>(PipeArgs);
+template __global__ void k_pipeline<128, true>(PipeArgs);
+template __global__ void k_pipeline<256, true>(PipeArgs);
 
-void* pipeline_kernel(int nsolve) {
-    return nsolve >= 256 ? reinterpret_cast<void*>(&k_pipeline<256>) : reinterpret_cast<void*>(&k_pipeline<128>);
+void* pipeline_kernel(int nsolve, bool trace) {
+    if (trace)
+        return nsolve >= 256 ? reinterpret_cast<void*>(&k_pipeline<256, true>)
+                             : reinterpret_cast<void*>(&k_pipeline<128, true>);
+    return nsolve >= 256 ? reinterpret_cast<void*>(&k_pipeline<256, false>)
+                         : reinterpret_cast<void*>(&k_pipeline<128, false>);
+}
+
+// Fill a mailbox array with the empty sentinel.
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+void fill_mailboxes(unsigned long long* p, long long n, cudaStream_t st) {
+    if (n <= 0) return;
+    k_fill_u64<<<296, 256, 0, st>>>(p, n, kEmpty);
 }
 
 }  // namespace hec::dev
