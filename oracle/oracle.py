@@ -36,6 +36,11 @@ class Csr:
     ci: np.ndarray
     v: np.ndarray
 
+    def __post_init__(self):
+        self.rp = np.ascontiguousarray(self.rp, dtype=I32)
+        self.ci = np.ascontiguousarray(self.ci, dtype=I32)
+        self.v = np.ascontiguousarray(self.v, dtype=F64)
+
     @property
     def n(self):
         return self.n_rows
