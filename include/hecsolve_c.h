@@ -104,11 +104,12 @@ int hec_tri_query(hec_tri_t t, hec_tri_info* info);
 int hec_tri_destroy(hec_tri_t t);
 
 /* Diagnostics (PIPELINE strategy): same as hec_tri_solve, and additionally
- * writes 8 uint64 per chunk into trace_dev (device, info.chunks * 8):
- * globaltimer ns at [0] blob issued, [1] b gather issued, [2] waiter start,
- * [3] waits cleared, [4] solvers start, [5] solvers done, [6] progress
- * published; [7] solver SM cycles. cta_chunk0 (host, ctas + 1) receives the
- * chunk range of every CTA. Either pointer may be NULL. */
+ * writes 64 uint64 per chunk into trace_dev (device, info.chunks * 64,
+ * zero-initialised): %globaltimer ns at [0] blob copy issued, [1] waiter sees
+ * the blob, [2] foreign values staged, [3] chunk ready; for solver warp w:
+ * [8+3w] ready seen, [9+3w] source warps done, [10+3w] segment done.
+ * cta_chunk0 (host, ctas + 1) receives the chunk range of every CTA. Either
+ * pointer may be NULL. */
 int hec_tri_solve_traced(hec_tri_t t, const double* b_dev, double* x_dev, void* stream,
                          unsigned long long* trace_dev, int* cta_chunk0);
 

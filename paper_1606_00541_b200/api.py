@@ -344,13 +344,13 @@ class DeviceTri:
         """Diagnostics: run one solve and return (trace[chunks, 8] uint64, cta_chunk0)."""
         import torch
         info = self.info()
-        trace = torch.zeros(max(info["chunks"], 1) * 16, dtype=torch.int64, device="cuda")
+        trace = torch.zeros(max(info["chunks"], 1) * 64, dtype=torch.int64, device="cuda")
         c0 = np.zeros(info["ctas"] + 1, dtype=_i32)
         check(lib.hec_tri_solve_traced(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(x_dev)),
                                        C.c_void_p(_stream(stream)) if stream is not None else None,
                                        C.c_void_p(_ptr(trace)), _p_int(c0)))
         torch.cuda.synchronize()
-        return trace.cpu().numpy().view(np.uint64).reshape(-1, 16)[:info["chunks"]], c0
+        return trace.cpu().numpy().view(np.uint64).reshape(-1, 64)[:info["chunks"]], c0
 
     def __del__(self):
         if getattr(self, "_h", None) and self._owner is None:

@@ -4,6 +4,8 @@
 #include "device_runtime.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "tri_kernels.cuh"
@@ -62,45 +64,48 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
 
     strategy_ = opt.strategy == 1 ? 1 : 2;
     if (strategy_ == 2 && n_ > 0) {
-        plan::PipelineConfig cfg;
+        plan::WaveConfig cfg;
         cfg.ctas = opt.ctas > 0 ? opt.ctas : sm_count();
-        plan::PipelineLayout P = plan::build_pipeline(src, cfg);
+        cfg.warps = kWaveSolverWarps;
+        cfg.warp_rows = 32;  // one row per lane
         const int budget = smem_optin() - 1024;  // static shared + slack
-        p_threads_ = opt.threads > 0 ? (opt.threads >= 256 ? 256 : 128) : (P.max_rows > 160 ? 256 : 128);
-        p_b_bytes_ = rup(8 * rup(std::max(P.max_rows, 1), 4), 128);
-        p_halo_bytes_ = rup(8 * std::max(P.max_halo, 1), 128);
-        p_slot_bytes_ = p_b_bytes_ + p_halo_bytes_ + rup(P.max_blob, 128);
-        p_ring_ = P.ring;
-        int ns = 0;
-        for (int k = 32; k >= 2; --k) {
-            const int ring_off = rup(24 * k, 16);  // 3 mbarriers per slot
-            const int slot_off = rup(ring_off + 8 * (p_ring_ + 1), 128);
-            if (slot_off + k * p_slot_bytes_ <= budget) {
-                ns = k;
-                p_ring_off_ = ring_off;
-                p_slot_off_ = slot_off;
-                break;
-            }
+        plan::WaveLayout P;
+        bool ok = true;
+        try {
+            P = plan::build_wave(src, cfg);
+        } catch (const std::invalid_argument&) {
+            ok = false;  // row order the wave layout cannot schedule: level launches
         }
-        if (ns >= 2) {
-            p_nslots_ = ns;
-            p_lag_ = std::max(1, ns / 2);
-            p_smem_ = p_slot_off_ + ns * p_slot_bytes_;
+        p_ring_ = cfg.ring;
+        p_ring_off_ = kWaveCtrlBytes;
+        p_buf_off_ = rup(p_ring_off_ + 8 * (p_ring_ + 1), 128);
+        p_buf_bytes_ = (budget - p_buf_off_) / 16 * 16;
+        if (ok && 2 * P.max_region <= p_buf_bytes_) {
+            p_warps_ = P.warps;
+            p_inflight_ = P.inflight;
+            p_lead_ = P.lead;
+            if (std::getenv("HEC_DEBUG"))
+                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d max_region=%d buf=%d exports=%lld "
+                             "deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n, P.chunks, P.ctas, P.warps,
+                             P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps, P.halo_deps,
+                             P.halo_values);
+            p_smem_ = p_buf_off_ + p_buf_bytes_;
             p_ctas_ = P.ctas;
-            p_kernel_ = pipeline_kernel(p_threads_, false);
-            p_kernel_trace_ = pipeline_kernel(p_threads_, true);
+            p_kernel_ = wave_kernel(P.max_width, false);
+            p_kernel_trace_ = wave_kernel(P.max_width, true);
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_trace_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
-            p_mailboxes_ = P.mailboxes;
+            p_exports_ = P.exports;
             p_blob_.upload(P.blob);
             p_spans_.upload(P.span);
             p_cta0_.upload(P.cta_chunk0);
             p_cta0_host_ = P.cta_chunk0;
             stats_.ctas = p_ctas_;
-            stats_.threads = p_threads_;
+            stats_.threads = kWaveRoleThreads + 32 * p_warps_;
             stats_.chunks = P.chunks;
-            stats_.slots = ns;
-            stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size());
+            stats_.slots = p_inflight_;
+            stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size() +
+                                                         16 * P.exports);
         } else {
             strategy_ = 1;  // a chunk too large for shared memory: level launches
         }
@@ -144,8 +149,8 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
         w = std::make_unique<Workspace>();
         w->counters.alloc(2);
         HEC_CUDA(cudaMemset(w->counters.p, 0, sizeof(uint32_t) * 2));
-        w->mailbox.alloc(static_cast<std::size_t>(std::max<long long>(p_mailboxes_, 1)));
-        fill_mailboxes(w->mailbox.p, static_cast<long long>(w->mailbox.count), nullptr);
+        w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
+        HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
         HEC_CUDA(cudaDeviceSynchronize());
     }
     return *w;
@@ -174,28 +179,32 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st,
         return;
     }
     Workspace& w = workspace(st);
-    PipeArgs a{};
+    if (++w.epoch == 0) {  // 2^32 solves on this stream: clear the mailboxes and restart the epochs
+        HEC_CUDA(cudaMemsetAsync(w.mailbox.p, 0, sizeof(unsigned long long) * w.mailbox.count, st));
+        w.epoch = 1;
+    }
+    WaveArgs a{};
     a.blobs = p_blob_.p;
-    a.spans = reinterpret_cast<const int2*>(p_spans_.p);
+    a.spans = reinterpret_cast<const int4*>(p_spans_.p);
     a.cta_chunk0 = p_cta0_.p;
     a.b = b;
     a.xs = xs;
     a.out = has_out_ ? out : nullptr;
     a.mbox = w.mailbox.p;
     a.counters = w.counters.p;
+    a.epoch = w.epoch;
     a.ctas = p_ctas_;
-    a.nslots = p_nslots_;
-    a.lag = p_lag_;
-    a.slot_bytes = p_slot_bytes_;
-    a.b_bytes = p_b_bytes_;
-    a.halo_bytes = p_halo_bytes_;
+    a.inflight = p_inflight_;
+    a.inflight_log2 = __builtin_ctz(static_cast<unsigned>(p_inflight_));
+    a.lead = p_lead_;
     a.ring = p_ring_;
     a.ring_off = p_ring_off_;
-    a.slot_off = p_slot_off_;
+    a.buf_off = p_buf_off_;
+    a.buf_bytes = p_buf_bytes_;
     a.trace = trace;
     void* args[] = {&a};
     HEC_CUDA(cudaLaunchKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_),
-                              dim3(kPipelineRoleThreads + p_threads_), args, p_smem_, st));
+                              dim3(kWaveRoleThreads + 32 * p_warps_), args, p_smem_, st));
 }
 
 void DeviceTri::solve_host(const double* b, double* x) {

@@ -91,7 +91,8 @@ public:
 private:
     struct Workspace {
         DevBuf<uint32_t> counters;            // ticket + finished CTAs
-        DevBuf<unsigned long long> mailbox;   // cross-CTA values (sentinel = empty)
+        DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
+        uint32_t epoch = 0;                   // last solve's epoch on this stream
     };
     Workspace& workspace(cudaStream_t st);
 
@@ -104,14 +105,14 @@ private:
     DevBuf<double> l_ell_val_, l_diag_, l_tail_val_;
     int l_width_ = 0, l_ld_ = 0;
     bool has_out_ = false;
-    // PIPELINE
+    // WAVE (persistent wavefront kernel)
     DevBuf<unsigned char> p_blob_;
     DevBuf<int> p_spans_, p_cta0_;
-    int p_ctas_ = 0, p_nslots_ = 0, p_lag_ = 0, p_slot_bytes_ = 0, p_b_bytes_ = 0, p_halo_bytes_ = 0;
-    int p_ring_ = 0, p_ring_off_ = 0, p_slot_off_ = 0, p_smem_ = 0, p_threads_ = 0;
+    int p_ctas_ = 0, p_inflight_ = 0, p_ring_ = 0, p_ring_off_ = 0, p_buf_off_ = 0, p_buf_bytes_ = 0;
+    int p_smem_ = 0, p_warps_ = 0, p_lead_ = 1;
     void* p_kernel_ = nullptr;
     void* p_kernel_trace_ = nullptr;
-    long long p_mailboxes_ = 0;
+    long long p_exports_ = 0;
     std::vector<int> p_cta0_host_;
 
     std::mutex mu_;

@@ -24,30 +24,33 @@ struct LevelArgs {
     int ld;
 };
 
-struct PipeArgs {
+struct WaveArgs {
     const unsigned char* blobs;  // all chunk blobs (16-byte aligned)
-    const int2* spans;           // per chunk (offset / 16, bytes)
+    const int4* spans;           // per chunk: (blob offset / 16, blob bytes, region bytes, 0)
     const int* cta_chunk0;       // ctas + 1
     const double* b;
     double* xs;
     double* out;
-    unsigned long long* mbox;    // cross-CTA mailbox words (sentinel = empty)
+    unsigned long long* mbox;    // 2 words per exported row: {lo32|epoch<<32, hi32|epoch<<32}
     uint32_t* counters;          // [0] ticket, [1] CTAs finished
+    uint32_t epoch;              // this solve's mailbox epoch (never 0)
     int ctas;
-    int nslots;
-    int lag;
-    int slot_bytes;
-    int b_bytes;                 // gathered-b area at the start of each slot
-    int halo_bytes;              // staged halo values after it
-    int ring;                    // ring entries (power of two)
+    int inflight;                // descriptor slots (power of two <= 32)
+    int inflight_log2;
+    int lead;                    // max chunks a warp runs ahead of the slowest warp
+    int ring;                    // x ring entries (power of two)
     int ring_off;                // shared-memory byte offsets
-    int slot_off;
+    int buf_off;
+    int buf_bytes;
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 
 void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
-void* pipeline_kernel(int nsolve, bool trace);
-void fill_mailboxes(unsigned long long* p, long long n, cudaStream_t st);
-constexpr int kPipelineRoleThreads = 64;  // producer warp + waiter warp
+// kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise)
+void* wave_kernel(int width, bool trace);
+constexpr int kWaveSolverWarps = 16;
+constexpr int kWaveWaiters = 3;                        // waiter warps
+constexpr int kWaveRoleThreads = 32 * (1 + kWaveWaiters);  // producer warp + waiter warps
+constexpr int kWaveCtrlBytes = 1536;                   // control block at the start of shared memory
 
 }  // namespace hec::dev

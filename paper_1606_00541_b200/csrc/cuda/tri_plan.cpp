@@ -116,42 +116,97 @@ LevelLayout build_levels(const TriSource& s) {
     return L;
 }
 
-PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
-    PipelineLayout P;
+WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
+    WaveLayout P;
     const int n = s.n;
     const int C = std::max(1, std::min(cfg.ctas, std::max(n, 1)));
+    const int NW = std::max(1, std::min(cfg.warps, 32));
+    const int R = cfg.ring;
     P.n = n;
     P.nlev = s.nlev;
     P.ctas = C;
-    P.ring = cfg.ring;
+    P.warps = NW;
+    P.ring = R;
+    P.inflight = cfg.inflight;
+    P.lead = std::max(1, std::min(cfg.lead, cfg.inflight));
     P.has_out = s.out_map != nullptr;
     const int per = n > 0 ? (n + C - 1) / C : 1;
+    const int per_w = (per + NW - 1) / NW;
     auto owner_of_i = [&](int i) { return std::min(i / per, C - 1); };
+    auto warp_of_i = [&](int i) { return std::min((i - owner_of_i(i) * per) / per_w, NW - 1); };
 
-    // 1. chunk discovery: level-major walk, runs of equal owner (split by size)
-    struct Chunk { int cta, level, r0, m, w, ntail; };
-    std::vector<int> cnt(n);
+    std::vector<int> cnt(n), owner_r(n), warp_r(n), nforeign(n, 0);
 #pragma omp parallel for schedule(static)
-    for (int r = 0; r < n; ++r) cnt[r] = entry_count(s, r);
+    for (int r = 0; r < n; ++r) {
+        cnt[r] = entry_count(s, r);
+        owner_r[r] = owner_of_i(s.inv_perm[r]);
+        warp_r[r] = warp_of_i(s.inv_perm[r]);
+    }
+    // foreign dependencies must come from lower CTAs (ticket order = forward progress)
+    bool bad = false;
+#pragma omp parallel for schedule(static) reduction(|| : bad)
+    for (int r = 0; r < n; ++r) {
+        int f = 0;
+        for_each_entry(s, r, [&](int col, double) {
+            if (owner_r[col] != owner_r[r]) {
+                ++f;
+                if (owner_r[col] > owner_r[r]) bad = true;
+            }
+        });
+        nforeign[r] = f;
+    }
+    if (bad) throw std::invalid_argument("hec_tri_create: wave layout needs dependencies on lower CTAs only");
 
+    // 0. one sliced-ELL width W for the whole layout (every chunk padded to W, so
+    //    the kernel's row loop is straight-line code): the supported width that
+    //    minimises ELL bytes + tail bytes (tail entries weighted double: they run
+    //    as a sequential loop)
+    {
+        const int cand[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 13, 16};
+        std::vector<long long> hist(cfg.max_width + 2, 0);
+        int maxc = 0;
+        for (int r = 0; r < n; ++r) {
+            ++hist[std::min(cnt[r], cfg.max_width + 1)];
+            maxc = std::max(maxc, cnt[r]);
+        }
+        long long best = -1;
+        P.max_width = 1;
+        for (int wc : cand) {
+            if (wc > cfg.max_width) break;
+            long long cost = 12LL * wc * n;
+            for (int k = wc + 1; k <= cfg.max_width + 1; ++k) cost += 24LL * (k - wc) * hist[k];
+            if (best < 0 || cost < best) {
+                best = cost;
+                P.max_width = wc;
+            }
+            if (wc >= maxc) break;
+        }
+    }
+    const int W = P.max_width;
+
+    // 1. chunk discovery: per level, the run of each CTA, split so that no warp
+    //    has more than warp_rows rows in a chunk and by bytes
+    struct Chunk { int level, r0, m, w, ntail; };
     std::vector<std::vector<Chunk>> per_cta(C);
-    const int flags_out = P.has_out ? 2 : 0;
+    const int fl_est = 4 | (P.has_out ? 2 : 0);
     for (int k = 0; k < s.nlev; ++k) {
         int r = s.level_starts[k];
         const int re = s.level_starts[k + 1];
         while (r < re) {
-            const int c = owner_of_i(s.inv_perm[r]);
-            Chunk ch{c, k, r, 0, 0, 0};
-            while (r < re && owner_of_i(s.inv_perm[r]) == c) {
-                const int w2 = std::max(ch.w, std::min(cnt[r], cfg.max_width));
-                const int t2 = ch.ntail + std::max(0, cnt[r] - cfg.max_width);
-                const int fl = (t2 > 0 ? 1 : 0) | flags_out | 4;
-                // blob + gathered b + (typical) one halo value and one mailbox per row
-                const int bytes = blob_sections(ch.m + 1, w2, ch.m + 1, ch.m + 1, t2, fl).end +
-                                  16 * round_up(ch.m + 1, 4);
-                if (ch.m > 0 && bytes > cfg.slot_cap) break;
-                ch.w = w2;
+            const int c = owner_r[r];
+            Chunk ch{k, r, 0, W, 0};
+            int halo_ub = 0, cur_w = -1, cur_cnt = 0;
+            while (r < re && owner_r[r] == c) {
+                const int t2 = ch.ntail + std::max(0, cnt[r] - W);
+                const int h2 = halo_ub + nforeign[r];
+                const int fl = fl_est | (t2 > 0 ? 1 : 0);
+                const int wcnt = warp_r[r] == cur_w ? cur_cnt + 1 : 1;
+                const int bytes = wave_region_bytes(ch.m + 1, h2, wave_sections(ch.m + 1, W, NW, h2, t2, fl).end);
+                if (ch.m > 0 && (wcnt > cfg.warp_rows || bytes > cfg.max_bytes)) break;
+                cur_w = warp_r[r];
+                cur_cnt = wcnt;
                 ch.ntail = t2;
+                halo_ub = h2;
                 ++ch.m;
                 ++r;
             }
@@ -159,179 +214,144 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
         }
     }
 
-    // 2. owner, sequence number and chunk position of every reordered row
-    std::vector<int> owner_r(n), seq_r(n), chunk_pos_r(n);
+    // 2. sequence numbers, chunk position, ring windows
+    std::vector<int> seq_r(n), chunk_pos_r(n);
+    std::vector<std::vector<int>> win(C), qend(C);
     P.cta_chunk0.assign(static_cast<std::size_t>(C) + 1, 0);
     for (int c = 0; c < C; ++c) {
-        P.cta_chunk0[c + 1] = P.cta_chunk0[c] + static_cast<int>(per_cta[c].size());
+        const auto& L = per_cta[c];
+        P.cta_chunk0[c + 1] = P.cta_chunk0[c] + static_cast<int>(L.size());
         int q = 0;
-        for (std::size_t j = 0; j < per_cta[c].size(); ++j) {
-            const Chunk& ch = per_cta[c][j];
-            for (int t = 0; t < ch.m; ++t) {
-                owner_r[ch.r0 + t] = c;
-                seq_r[ch.r0 + t] = q + t;
-                chunk_pos_r[ch.r0 + t] = static_cast<int>(j);
+        qend[c].resize(L.size());
+        for (std::size_t j = 0; j < L.size(); ++j) {
+            for (int t = 0; t < L[j].m; ++t) {
+                seq_r[L[j].r0 + t] = q + t;
+                chunk_pos_r[L[j].r0 + t] = static_cast<int>(j);
             }
-            q += ch.m;
+            q += L[j].m;
+            qend[c][j] = q;
+        }
+        // a warp may run up to lead-1 chunks ahead of the slowest one: ring
+        // entries newer than q_end(j) - win(j) cannot have been overwritten yet
+        win[c].resize(L.size());
+        for (std::size_t j = 0; j < L.size(); ++j) {
+            const std::size_t last = std::min(L.size() - 1, j + static_cast<std::size_t>(P.lead) - 1);
+            win[c][j] = R - (qend[c][last] - qend[c][j]);
         }
     }
     P.chunks = P.cta_chunk0[C];
 
-    // 3. consumer side (parallel over CTAs): dependency codes, per-chunk halo
-    //    lists and the CTA's mailboxes (one per foreign producer row).
-    struct CtaWork {
-        std::vector<std::vector<int>> dep, tdep, tptr, halo;  // per chunk
-        std::vector<std::vector<double>> val, tval;
-        std::vector<int> mb_row;        // local mailbox -> producer reordered row
-        std::vector<int> mb_last;       // local mailbox -> last chunk that reads it
-        std::vector<char> has_global;   // per chunk: some dependency read from global x
-        long long ring_deps = 0, global_deps = 0, halo_deps = 0;
-        bool bad = false;
-    };
-    std::vector<CtaWork> work(C);
+    // 3. exports: rows read by another CTA get a mailbox id
+    std::vector<int> export_id(n, -1);
+    {
+        std::vector<char> exported(n, 0);
+#pragma omp parallel for schedule(static)
+        for (int r = 0; r < n; ++r)
+            if (nforeign[r])
+                for_each_entry(s, r, [&](int col, double) {
+                    if (owner_r[col] != owner_r[r]) exported[col] = 1;  // benign race: all write 1
+                });
+        long long e = 0;
+        for (int r = 0; r < n; ++r)
+            if (exported[r]) export_id[r] = static_cast<int>(e++);
+        if (e > 0x7ffffffeLL) throw std::overflow_error("hec_tri_create: too many exported rows");
+        P.exports = e;
+    }
+
+    // 4. emit blobs (parallel over CTAs)
+    std::vector<std::vector<unsigned char>> cta_blob(C);
+    std::vector<std::vector<int>> cta_span(C);
+    std::vector<int> region_max(C, 0);
+    std::vector<long long> st_ring(C, 0), st_glob(C, 0), st_halo(C, 0), st_hval(C, 0);
+    std::vector<char> seg_bad(C, 0);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int c = 0; c < C; ++c) {
-        CtaWork& W = work[c];
-        const std::size_t nchk = per_cta[c].size();
-        W.dep.resize(nchk);
-        W.val.resize(nchk);
-        W.tdep.resize(nchk);
-        W.tval.resize(nchk);
-        W.tptr.resize(nchk);
-        W.halo.resize(nchk);
-        W.has_global.assign(nchk, 0);
-        std::unordered_map<int, int> mb_of;   // producer row -> local mailbox
-        std::unordered_map<int, int> halo_of; // local mailbox -> halo slot (this chunk)
-        int q0 = 0;
-        for (std::size_t j = 0; j < nchk; ++j) {
-            const Chunk& ch = per_cta[c][j];
-            const int q_end = q0 + ch.m;
+        const auto& L = per_cta[c];
+        auto& out = cta_blob[c];
+        cta_span[c].resize(4 * L.size());
+        std::unordered_map<int, int> halo_of;
+        std::vector<int> halo, dep, tptr, tdep;
+        std::vector<double> val, tval;
+        for (std::size_t j = 0; j < L.size(); ++j) {
+            const Chunk& ch = L[j];
             const int m = ch.m, w = ch.w, mp = round_up(m, 4);
+            const int q0 = qend[c][j] - m;
+            const int lo = qend[c][j] - win[c][j];
             halo_of.clear();
-            auto& halo = W.halo[j];
-            auto encode = [&](int col) -> int {
-                const int oc = owner_r[col];
-                if (oc == c) {
-                    if (chunk_pos_r[col] >= static_cast<int>(j)) W.bad = true;
-                    if (seq_r[col] >= q_end - cfg.ring) {
-                        ++W.ring_deps;
-                        return -((seq_r[col] & (cfg.ring - 1)) + 1);
-                    }
-                    ++W.global_deps;
-                    W.has_global[j] = 1;
-                    return sol_index(s, col);
-                }
-                if (oc > c) W.bad = true;
-                auto it = mb_of.find(col);
-                int mb;
-                if (it == mb_of.end()) {
-                    mb = static_cast<int>(W.mb_row.size());
-                    mb_of.emplace(col, mb);
-                    W.mb_row.push_back(col);
-                    W.mb_last.push_back(static_cast<int>(j));
-                } else {
-                    mb = it->second;
-                    W.mb_last[mb] = static_cast<int>(j);
-                }
-                auto hit = halo_of.find(mb);
-                int h;
-                if (hit == halo_of.end()) {
-                    h = static_cast<int>(halo.size());
-                    halo_of.emplace(mb, h);
-                    halo.push_back(mb);
-                } else {
-                    h = hit->second;
-                }
-                ++W.halo_deps;
-                return -(cfg.ring + 2 + h);
-            };
-            auto& dep = W.dep[j];
-            auto& val = W.val[j];
-            auto& tptr = W.tptr[j];
-            dep.assign(static_cast<std::size_t>(w) * mp, -(cfg.ring + 1));
+            halo.clear();
+            dep.assign(static_cast<std::size_t>(w) * mp, R);
             val.assign(static_cast<std::size_t>(w) * mp, 0.0);
             tptr.assign(round_up(mp + 1, 4), 0);
+            tdep.clear();
+            tval.clear();
+            std::vector<unsigned> mask(NW, 0u);
+            std::vector<int> t0(NW, -1), t1(NW, -1);
+            bool glob = false, any_exp = false;
             for (int t = 0; t < m; ++t) {
                 const int r = ch.r0 + t;
+                const int wr = warp_r[r];
+                if (t0[wr] < 0) t0[wr] = t;
+                else if (t1[wr] != t) seg_bad[c] = 1;  // warp rows must be contiguous in the chunk
+                t1[wr] = t + 1;
+                if (export_id[r] >= 0) any_exp = true;
                 int e = 0;
                 for_each_entry(s, r, [&](int col, double v) {
-                    const int d = encode(col);
+                    int d;
+                    if (owner_r[col] == c) {
+                        if (chunk_pos_r[col] >= static_cast<int>(j)) seg_bad[c] = 1;
+                        if (warp_r[col] != wr) mask[wr] |= 1u << warp_r[col];
+                        if (seq_r[col] >= lo) {
+                            d = seq_r[col] & (R - 1);
+                            ++st_ring[c];
+                        } else {
+                            d = -(sol_index(s, col) + 1);
+                            glob = true;
+                            ++st_glob[c];
+                        }
+                    } else {
+                        const int id = export_id[col];
+                        auto it = halo_of.find(id);
+                        int h;
+                        if (it == halo_of.end()) {
+                            h = static_cast<int>(halo.size());
+                            halo_of.emplace(id, h);
+                            halo.push_back(id);
+                        } else {
+                            h = it->second;
+                        }
+                        d = R + 1 + h;
+                        ++st_halo[c];
+                    }
                     if (e < w) {
                         dep[static_cast<std::size_t>(e) * mp + t] = d;
                         val[static_cast<std::size_t>(e) * mp + t] = v;
                     } else {
-                        W.tdep[j].push_back(d);
-                        W.tval[j].push_back(v);
+                        tdep.push_back(d);
+                        tval.push_back(v);
                     }
                     ++e;
                 });
-                tptr[t + 1] = static_cast<int>(W.tdep[j].size());
+                tptr[t + 1] = static_cast<int>(tdep.size());
             }
             for (int t = m; t < static_cast<int>(tptr.size()) - 1; ++t) tptr[t + 1] = tptr[t];
-            q0 = q_end;
-        }
-    }
-    for (int c = 0; c < C; ++c)
-        if (work[c].bad) throw std::invalid_argument("hec_tri_create: dependency order violates the level schedule");
-
-    // 4. global mailbox ids and the producer-side lists (reordered row -> ids)
-    std::vector<long long> mb_base(static_cast<std::size_t>(C) + 1, 0);
-    for (int c = 0; c < C; ++c) mb_base[c + 1] = mb_base[c] + static_cast<long long>(work[c].mb_row.size());
-    P.mailboxes = mb_base[C];
-    if (P.mailboxes > 0x3fffffffLL) throw std::overflow_error("hec_tri_create: too many cross-CTA values");
-    std::vector<int> feed_ptr(static_cast<std::size_t>(n) + 1, 0);
-    for (int c = 0; c < C; ++c)
-        for (int r : work[c].mb_row) ++feed_ptr[r + 1];
-    for (int r = 0; r < n; ++r) feed_ptr[r + 1] += feed_ptr[r];
-    std::vector<int> feed(static_cast<std::size_t>(feed_ptr[n]));
-    {
-        std::vector<int> fill(feed_ptr.begin(), feed_ptr.end() - 1);
-        for (int c = 0; c < C; ++c)
-            for (std::size_t l = 0; l < work[c].mb_row.size(); ++l)
-                feed[fill[work[c].mb_row[l]]++] = static_cast<int>(mb_base[c] + static_cast<long long>(l));
-    }
-
-    // 5. emit blobs (parallel over CTAs)
-    P.span.assign(2 * static_cast<std::size_t>(P.chunks), 0);
-    std::vector<std::vector<unsigned char>> cta_blob(C);
-    std::vector<int> blob_max(C, 0), rows_max(C, 0), halo_max(C, 0);
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int c = 0; c < C; ++c) {
-        CtaWork& W = work[c];
-        auto& out = cta_blob[c];
-        int q0 = 0;
-        for (std::size_t j = 0; j < per_cta[c].size(); ++j) {
-            const Chunk& ch = per_cta[c][j];
-            const int m = ch.m, w = ch.w, mp = round_up(m, 4);
-            std::vector<int> mbptr(round_up(mp + 1, 4), 0), mbid;
-            for (int t = 0; t < m; ++t) {
-                const int r = ch.r0 + t;
-                for (int k = feed_ptr[r]; k < feed_ptr[r + 1]; ++k) mbid.push_back(feed[k]);
-                mbptr[t + 1] = static_cast<int>(mbid.size());
-            }
-            for (int t = m; t < static_cast<int>(mbptr.size()) - 1; ++t) mbptr[t + 1] = mbptr[t];
-            const int nmb = static_cast<int>(mbid.size());
-            const int nhalo = static_cast<int>(W.halo[j].size());
-            const int ntail = static_cast<int>(W.tdep[j].size());
-            const int flags = (ntail > 0 ? 1 : 0) | flags_out | (nmb > 0 ? 4 : 0) | (W.has_global[j] ? 8 : 0);
-            const BlobSections sec = blob_sections(m, w, nhalo, nmb, ntail, flags);
+            const int nhalo = static_cast<int>(halo.size());
+            const int ntail = static_cast<int>(tdep.size());
+            st_hval[c] += nhalo;
+            (void)any_exp;  // the export list is always present (-1 = row not exported)
+            const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0);
+            const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
+            const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
-            out.resize(base + sec.end, 0);
+            out.resize(base + round_up(sec.end, 16), 0);
             unsigned char* b = out.data() + base;
-            const ChunkHeader hdr{m,        w,         q0,       flags,    nhalo,    ntail,     nmb,
-                                  mp,       sec.halo,  sec.mbptr, sec.mbid, sec.diag, sec.val,   sec.dep,
-                                  sec.bidx, sec.xidx,  sec.oidx, sec.tptr, sec.tval, sec.tdep, {0, 0, 0, 0}};
+            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, round_up(sec.end, 16)};
             std::memcpy(b, &hdr, sizeof(hdr));
-            for (int h = 0; h < nhalo; ++h) {
-                const int l = W.halo[j][h];
-                const long long gid = mb_base[c] + l;
-                const int code = static_cast<int>(gid * 2 + (W.mb_last[l] == static_cast<int>(j) ? 1 : 0));
-                std::memcpy(b + sec.halo + 4 * h, &code, 4);
+            for (int wi = 0; wi < NW; ++wi) {
+                const unsigned a = t0[wi] < 0 ? 0u : (static_cast<unsigned>(t0[wi]) | (static_cast<unsigned>(t1[wi]) << 16));
+                std::memcpy(b + sec.seg + 8 * wi, &a, 4);
+                std::memcpy(b + sec.seg + 8 * wi + 4, &mask[wi], 4);
             }
-            if (flags & 4) {
-                std::memcpy(b + sec.mbptr, mbptr.data(), 4 * mbptr.size());
-                std::memcpy(b + sec.mbid, mbid.data(), 4 * mbid.size());
-            }
+            if (nhalo) std::memcpy(b + sec.halo, halo.data(), 4 * nhalo);
             auto put_i = [&](int off, int idx, int v) { std::memcpy(b + off + 4 * idx, &v, 4); };
             auto put_d = [&](int off, int idx, double v) { std::memcpy(b + off + 8 * idx, &v, 8); };
             for (int t = 0; t < m; ++t) {
@@ -341,28 +361,31 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
                 put_i(sec.bidx, t, s.b_map ? s.b_map[o] : o);
                 put_i(sec.xidx, t, o);
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
+                put_i(sec.exp, t, export_id[r]);
             }
-            std::memcpy(b + sec.val, W.val[j].data(), 8 * W.val[j].size());
-            std::memcpy(b + sec.dep, W.dep[j].data(), 4 * W.dep[j].size());
+            for (int t = m; t < mp; ++t) {  // padded rows: harmless values
+                put_d(sec.diag, t, 1.0);
+                put_i(sec.bidx, t, 0);
+                put_i(sec.exp, t, -1);
+            }
+            std::memcpy(b + sec.val, val.data(), 8 * val.size());
+            std::memcpy(b + sec.dep, dep.data(), 4 * dep.size());
             if (flags & 1) {
-                std::memcpy(b + sec.tptr, W.tptr[j].data(), 4 * W.tptr[j].size());
-                std::memcpy(b + sec.tval, W.tval[j].data(), 8 * W.tval[j].size());
-                std::memcpy(b + sec.tdep, W.tdep[j].data(), 4 * W.tdep[j].size());
+                std::memcpy(b + sec.tptr, tptr.data(), 4 * tptr.size());
+                std::memcpy(b + sec.tval, tval.data(), 8 * tval.size());
+                std::memcpy(b + sec.tdep, tdep.data(), 4 * tdep.size());
             }
-            blob_max[c] = std::max(blob_max[c], sec.end);
-            rows_max[c] = std::max(rows_max[c], m);
-            halo_max[c] = std::max(halo_max[c], nhalo);
-            const int gj = P.cta_chunk0[c] + static_cast<int>(j);
-            P.span[2 * gj + 0] = static_cast<int>(base / 16);  // CTA-relative for now
-            P.span[2 * gj + 1] = sec.end;
-            q0 += m;
-            // free the consumer-side scratch as we go
-            std::vector<int>().swap(W.dep[j]);
-            std::vector<double>().swap(W.val[j]);
+            region_max[c] = std::max(region_max[c], region);
+            cta_span[c][4 * j + 0] = static_cast<int>(base / 16);  // CTA-relative for now
+            cta_span[c][4 * j + 1] = round_up(sec.end, 16);
+            cta_span[c][4 * j + 2] = region;
+            cta_span[c][4 * j + 3] = 8 * mp;
         }
     }
+    for (int c = 0; c < C; ++c)
+        if (seg_bad[c]) throw std::invalid_argument("hec_tri_create: dependency order violates the level schedule");
 
-    // 6. concatenate CTA streams (16-byte aligned offsets)
+    // 5. concatenate CTA streams
     std::size_t total = 0;
     std::vector<std::size_t> cta_base(C);
     for (int c = 0; c < C; ++c) {
@@ -371,17 +394,22 @@ PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg) {
     }
     if (total / 16 > 0x7fffffffULL) throw std::overflow_error("hec_tri_create: layout exceeds 32 GiB");
     P.blob.resize(total);
+    P.span.assign(4 * static_cast<std::size_t>(P.chunks), 0);
     for (int c = 0; c < C; ++c) {
         std::memcpy(P.blob.data() + cta_base[c], cta_blob[c].data(), cta_blob[c].size());
         std::vector<unsigned char>().swap(cta_blob[c]);
-        for (int gj = P.cta_chunk0[c]; gj < P.cta_chunk0[c + 1]; ++gj)
-            P.span[2 * gj] += static_cast<int>(cta_base[c] / 16);
-        P.max_blob = std::max(P.max_blob, blob_max[c]);
-        P.max_rows = std::max(P.max_rows, rows_max[c]);
-        P.max_halo = std::max(P.max_halo, halo_max[c]);
-        P.ring_deps += work[c].ring_deps;
-        P.global_deps += work[c].global_deps;
-        P.halo_deps += work[c].halo_deps;
+        for (int j = 0; j < P.cta_chunk0[c + 1] - P.cta_chunk0[c]; ++j) {
+            const int g = P.cta_chunk0[c] + j;
+            P.span[4 * g + 0] = cta_span[c][4 * j] + static_cast<int>(cta_base[c] / 16);
+            P.span[4 * g + 1] = cta_span[c][4 * j + 1];
+            P.span[4 * g + 2] = cta_span[c][4 * j + 2];
+            P.span[4 * g + 3] = cta_span[c][4 * j + 3];
+        }
+        P.max_region = std::max(P.max_region, region_max[c]);
+        P.ring_deps += st_ring[c];
+        P.global_deps += st_glob[c];
+        P.halo_deps += st_halo[c];
+        P.halo_values += st_hval[c];
     }
     return P;
 }

@@ -52,94 +52,106 @@ struct LevelLayout {
 };
 LevelLayout build_levels(const TriSource& s);
 
-// -------------------------------------------------------------- PIPELINE ----
-// Persistent kernel, CTA c owns lower-frame rows [c*per, (c+1)*per). Its rows
-// of one level form a contiguous reordered range ("chunk"); chunks are laid out
-// back to back per CTA as self-describing 16-byte-aligned blobs that one
-// cp.async.bulk moves into shared memory.
+// ------------------------------------------------------------------ WAVE ----
+// Persistent wavefront kernel (one CTA per SM). CTA c owns the lower-frame
+// rows [c*per, (c+1)*per); inside the CTA, solver warp w owns the sub-range
+// [w*per_w, (w+1)*per_w). The CTA's rows of one level form a "chunk" (split
+// when large); because a level is sorted by lower-frame index
+// (reference level_schedule.cpp:51-56) a chunk is one contiguous reordered
+// range and each warp's rows in it are one contiguous segment.
 //
-// Cross-CTA values travel through MAILBOXES: one FP64 word per (producer row,
-// consumer CTA) pair. The producing solver thread stores x there (plain store,
-// no fence); the consumer's waiter warp polls the word until it no longer holds
-// the sentinel (a signalling NaN, which IEEE arithmetic can never produce),
-// stages it into shared memory, and re-arms the word with the sentinel after
-// its last use in this solve. No progress counters, no release/acquire fences.
+// Synchronisation replaces the reference's per-level barrier
+// (triangular.cpp:128) by dataflow:
+//   * inside a CTA: per-warp progress counters in shared memory; a warp
+//     starts its segment of chunk j once every warp it reads from (the
+//     segment's source mask) has finished chunk j-1;
+//   * across CTAs: rows read by another CTA are "exported": the producing
+//     thread writes the value into a 16-byte mailbox as two 8-byte words
+//     {lo32 | epoch, hi32 | epoch}; the consumer's waiter warps poll until
+//     both words carry the current solve's epoch, then stage the value in
+//     shared memory. Epochs advance per solve, so mailboxes are never reset.
+// Own-CTA values come from a shared-memory ring indexed by the CTA's row
+// sequence number; values older than the ring window are re-read from x.
+// No warp runs more than `lead`-1 chunks ahead of the slowest one, so an entry
+// read in chunk j is safe in the ring while it is newer than
+// q_end(j) - (R - rows of chunks j+1 .. j+lead-1).
 //
-// Blob layout (mp = round_up(m, 4)):
-//   ChunkHeader (96 B: counts + every section offset, so the device decodes a
-//                chunk with six 16-byte shared loads)
-//                flags: 1 tail, 2 out-map, 4 mailbox stores, 8 global deps
-//   int   halo[nhalo]   mailbox id * 2 + (1 if last use -> re-arm), pad 16 B
-//   int   mbptr[mp+1]   (flags & 4) per-row range into mbid, pad 16 B
-//   int   mbid[nmb]     (flags & 4) mailbox ids this chunk's rows feed, pad 16 B
+// Blob of one chunk (16-byte aligned, moved by one cp.async.bulk); mp =
+// round_up(m, 4), W = the layout's sliced-ELL width, NW = solver warps. Every
+// section before the tail sits at an offset computable from mp alone, so the
+// kernel reads only the 32-byte header and its warp's descriptor:
+//   WaveHeader (32 B)  {m, mp, q0, flags}, {nhalo, halo list, tail, bytes}
+//   uint2 seg[NW]        per solver warp: (t0 | t1 << 16, source-warp mask)
 //   double diag[mp]
-//   double val[w][mp]               sliced ELL, slot-major
-//   int    dep[w][mp]               >= 0 solution index (global, own rows older than the ring)
-//                                    < 0: s = -d-1; s < ring: x ring slot; s == ring: 0.0;
-//                                         s > ring: staged halo value s-ring-1
-//   int    bidx[mp], xidx[mp], (oidx[mp] if flags & 2)
-//   if flags & 1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
-// Shared-memory footprint of a chunk = blob + 8 * mp (gathered b) + 8 * nhalo.
-constexpr unsigned long long kMailboxEmpty = 0x7FF4DEADBEEF0001ULL;  // signalling NaN
-
-struct PipelineConfig {
+//   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep R)
+//   int    dep[W][mp]    0 <= d < R: ring slot; d == R: 0.0 (padding);
+//                        d > R: staged halo value d-R-1; d < 0: x[-d-1]
+//   int bidx[mp], xidx[mp], exp[mp] (mailbox id or -1), (oidx[mp] if flags&2)
+//   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
+//   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages
+// The shared-memory region of a chunk is [b: 8*mp][blob][staged halo: 8*nhalo];
+// the kernel addresses it from the blob start (b at -8*mp, halo at +bytes).
+struct WaveConfig {
     int ctas = 148;
-    int ring = 4096;          // x ring entries (power of two); slot `ring` holds 0.0
-    int max_width = 32;       // sliced-ELL width cap; longer rows spill to the tail
-    int slot_cap = 24576;     // target shared-memory bytes of one chunk
+    int warps = 8;            // solver warps per CTA (<= 32)
+    int warp_rows = 64;       // max rows of one warp in one chunk (32 * rows per lane)
+    int ring = 8192;          // x ring entries (power of two); slot `ring` holds 0.0
+    int inflight = 16;        // max chunks in flight per CTA (descriptor slots)
+    int lead = 4;             // a warp starts chunk j only after every warp finished chunk j-lead
+    int max_bytes = 40960;    // chunk split: shared-memory region bytes
+    int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
 };
 
-struct PipelineLayout {
-    int n = 0, nlev = 0, ctas = 0, ring = 0;
-    int max_blob = 0;                     // bytes of the largest blob
+struct WaveLayout {
+    int n = 0, nlev = 0, ctas = 0, warps = 0, ring = 0, inflight = 0, lead = 0;
     int chunks = 0;
-    int max_rows = 0;                     // rows of the largest chunk
-    int max_halo = 0;                     // halo values of the largest chunk
+    int max_region = 0;                   // bytes of the largest chunk region
+    int max_width = 0;                    // sliced-ELL width W of every chunk
+    long long exports = 0;                // mailboxes
     bool has_out = false;
-    long long mailboxes = 0;              // (producer row, consumer CTA) words
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
-    std::vector<int> span;                // 2 per chunk: (offset / 16, bytes)
+    std::vector<int> span;                // 4 per chunk: blob offset / 16, blob bytes, region bytes, b bytes
     std::vector<unsigned char> blob;      // all chunk blobs, 16-byte aligned
-    long long ring_deps = 0, global_deps = 0, halo_deps = 0;
+    long long ring_deps = 0, global_deps = 0, halo_deps = 0, halo_values = 0;
 };
-PipelineLayout build_pipeline(const TriSource& s, const PipelineConfig& cfg);
+WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg);
 
-// Blob section offsets (bytes from the blob start).
-struct BlobSections {
-    int halo, mbptr, mbid, diag, val, dep, bidx, xidx, oidx, tptr, tval, tdep, end;
+struct WaveSections {
+    int seg, diag, val, dep, bidx, xidx, exp, oidx, tptr, tval, tdep, halo, end;
 };
 
-// First 96 bytes of every blob; read by the kernel as-is.
-struct ChunkHeader {
-    int m, w, q0, flags;
-    int nhalo, ntail, nmb, mp;
-    int halo, mbptr, mbid, diag;
-    int val, dep, bidx, xidx;
-    int oidx, tptr, tval, tdep;
-    int pad[4];
+// First 32 bytes of every blob; read by the kernel as-is.
+struct WaveHeader {
+    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo
+    int nhalo, halo, tptr, bytes;  // halo id list / tail offsets, blob bytes (= staged halo offset)
 };
-static_assert(sizeof(ChunkHeader) == 96, "chunk header is six 16-byte words");
-constexpr int kChunkHeaderBytes = 96;
+static_assert(sizeof(WaveHeader) == 32, "wave header is two 16-byte words");
+constexpr int kWaveHeaderBytes = 32;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
-inline BlobSections blob_sections(int m, int w, int nhalo, int nmb, int ntail, int flags) {
-    BlobSections b{};
+// Offsets of the fixed sections (also computed this way on the device).
+inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, int flags) {
+    WaveSections b{};
     const int mp = round_up(m, 4);
-    int at = kChunkHeaderBytes;
-    b.halo = at;  at += round_up(4 * nhalo, 16);
-    b.mbptr = at; if (flags & 4) at += 4 * round_up(mp + 1, 4);
-    b.mbid = at;  if (flags & 4) at += round_up(4 * nmb, 16);
+    int at = kWaveHeaderBytes;
+    b.seg = at;   at += round_up(8 * nw, 16);
     b.diag = at;  at += 8 * mp;
     b.val = at;   at += 8 * mp * w;
     b.dep = at;   at += 4 * mp * w;
     b.bidx = at;  at += 4 * mp;
     b.xidx = at;  at += 4 * mp;
+    b.exp = at;   at += 4 * mp;
     b.oidx = at;  if (flags & 2) at += 4 * mp;
     b.tptr = at;  if (flags & 1) at += 4 * round_up(mp + 1, 4);
     b.tval = at;  if (flags & 1) at += 8 * round_up(ntail, 2);
     b.tdep = at;  if (flags & 1) at += 4 * round_up(ntail, 4);
+    b.halo = at;  at += 4 * round_up(nhalo, 4);
     b.end = at;
     return b;
+}
+// shared-memory bytes of a chunk region: gathered b + blob + staged halo
+inline int wave_region_bytes(int m, int nhalo, int blob_bytes) {
+    return 8 * round_up(m, 4) + round_up(blob_bytes, 16) + round_up(8 * nhalo, 16);
 }
 
 }  // namespace hec::plan

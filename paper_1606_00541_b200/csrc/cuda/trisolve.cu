@@ -10,18 +10,17 @@
 // Two strategies:
 //  * k_level_rows   one launch per level, thread per reordered row (baseline;
 //                   the reference's level barrier becomes a kernel boundary).
-//  * k_pipeline     persistent, one CTA per SM. CTA c owns a contiguous block of
-//                   lower-frame rows; its rows of level k form one chunk. Warp
-//                   roles: 0 = producer (cp.async.bulk of the next chunk blobs
-//                   into a shared-memory slot ring + cp.async gather of b),
-//                   1 = waiter (polls the mailbox words carrying the foreign x
-//                   values a chunk needs and stages them in shared memory),
-//                   2.. = solvers (own recent x values from a shared-memory
-//                   ring; foreign ones from the staged halo). The reference's
-//                   level barrier becomes a per-value dataflow handoff: the
-//                   producing thread's plain 8-byte store IS the signal (the
-//                   empty sentinel is a signalling NaN no arithmetic result can
-//                   equal), so no fence or flag sits on the critical path.
+//  * k_wave         persistent wavefront, one CTA per SM (tri_plan.hpp). CTA c
+//                   owns a contiguous block of lower-frame rows, each solver
+//                   warp a fixed slice of it. Warp roles: 0 = producer (byte-
+//                   ring allocation + cp.async.bulk of chunk blobs into shared
+//                   memory), 1..kWaveWaiters = waiters (cp.async gather of b,
+//                   polling of the epoch-tagged mailboxes that carry values
+//                   from lower CTAs), the rest = solvers. The reference's
+//                   per-level barrier becomes dataflow: a warp starts its part
+//                   of level k as soon as the warps it reads from finished
+//                   level k-1 (shared-memory progress counters) and the
+//                   foreign values are staged; no grid or CTA barrier.
 
 #include <cuda_runtime.h>
 
@@ -124,240 +123,343 @@ void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, c
     }
 }
 
-// ------------------------------------------------------------ PIPELINE ----
-using plan::ChunkHeader;
-constexpr unsigned long long kEmpty = plan::kMailboxEmpty;
+// ------------------------------------------------------------------ WAVE ----
+using plan::WaveHeader;
 
-// Shared-memory word of dependency code d < 0 (see tri_plan.hpp): the own-x
-// ring, its zero slot, or -- beyond the zero slot -- the chunk's staged halo,
-// which sits `hoff` doubles further from the ring base.
-__device__ __forceinline__ int smem_word(int d, int ring_n, int hoff) {
-    const int s = -d - 1;
-    return s + (s > ring_n ? hoff : 0);
-}
-
-// Any dependency code, including d >= 0 (own rows older than the ring: global x).
-__device__ __forceinline__ double dep_value(int d, const double* xs, const double* ring, int ring_n, int hoff) {
-    double v = ring[d < 0 ? smem_word(d, ring_n, hoff) : 0];
-    if (d >= 0) v = xs[d];
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint2 ld_volatile_v2(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_v2(uint2* p, uint32_t x, uint32_t y) {
+    asm volatile("st.volatile.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_u32(p)), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2(const unsigned long long* p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_v2(unsigned long long* p, unsigned long long lo, unsigned long long hi) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(lo), "l"(hi) : "memory");
+}
 
-// acc -= sum over W sliced-ELL slots, all loads issued before the FP chain.
+// Mailbox words carry 32 value bits and the solve's epoch each, so one
+// 8-byte single-copy-atomic word never mixes two solves.
+__device__ __forceinline__ bool mail_ok(ulonglong2 v, uint32_t ep) {
+    return static_cast<uint32_t>(v.x >> 32) == ep && static_cast<uint32_t>(v.y >> 32) == ep;
+}
+__device__ __forceinline__ double mail_value(ulonglong2 v) {
+    return __longlong_as_double(static_cast<long long>((v.y << 32) | (v.x & 0xffffffffULL)));
+}
+__device__ __forceinline__ void mail_store(unsigned long long* box, double x, uint32_t ep) {
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned long long tag = static_cast<unsigned long long>(ep) << 32;
+    st_relaxed_v2(box, (bits & 0xffffffffULL) | tag, (bits >> 32) | tag);
+}
+
+// x = a / d, correctly rounded, with y = RN(1/d) computed off the critical
+// path: q = RN(a y), r = a - d q (exact), q' = RN(q + r y) is RN(a/d) while a
+// and q' stay clear of the under/overflow ranges (Markstein; the same tail as
+// the CUDA __ddiv_rn fast path, fed a correctly rounded reciprocal). Outside
+// the guard -- zeros, huge/tiny operands, Inf/NaN -- the IEEE division runs.
+// tools/markstein_check.c sweeps the identity on the host.
+__device__ __noinline__ double div_slow(double a, double d) { return __ddiv_rn(a, d); }
+__device__ __forceinline__ double div_rn(double a, double d, double y) {
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-d, q, a);
+    const double q1 = __fma_rn(r, y, q);
+    const double aa = fabs(a), aq = fabs(q1);
+    if (__builtin_expect(aa > 0x1p-900 && aa < 0x1p900 && aq > 0x1p-900 && aq < 0x1p900, 1)) return q1;
+    return div_slow(a, d);
+}
+
+// Dependency value (see tri_plan.hpp): ring / zero slot / staged halo live in
+// shared memory at ring_s + 8 d (d <= R) or hb_s + 8 d (d > R); d < 0 is x[-d-1].
+__device__ __forceinline__ uint32_t dep_addr(int d, int R, uint32_t ring_s, uint32_t hb_s) {
+    return (d <= R ? ring_s : hb_s) + 8u * static_cast<uint32_t>(d);
+}
+__device__ __forceinline__ double dep_value(int d, int R, uint32_t ring_s, uint32_t hb_s, const double* xs) {
+    return d >= 0 ? lds_f64(dep_addr(d, R, ring_s, hb_s)) : __ldcg(xs + (-d - 1));
+}
+
+// acc -= v[u] * x[dep[u]] for the W sliced-ELL slots of row t (padding slots
+// hold 0 * 0.0, which leaves acc bitwise unchanged), products formed first,
+// then the subtractions in slot order (reference triangular.cpp:118-122).
 template <int W>
-__device__ __forceinline__ double accumulate_fixed(double acc, const int* dep, const double* val, int mp, int t,
-                                                   const double* ring, int ring_n, int hoff) {
-    double xv[W], vv[W];
+__device__ __forceinline__ double accumulate(double acc, const int* dep, const double* val, int mp, int t, int R,
+                                             uint32_t ring_s, uint32_t hb_s, const double* xs, bool global) {
+    double p[W];
 #pragma unroll
     for (int u = 0; u < W; ++u) {
-        xv[u] = ring[smem_word(dep[u * mp + t], ring_n, hoff)];
-        vv[u] = val[u * mp + t];
+        const int d = dep[u * mp + t];
+        double xv;
+        if (global) xv = dep_value(d, R, ring_s, hb_s, xs);
+        else xv = lds_f64(dep_addr(d, R, ring_s, hb_s));
+        p[u] = __dmul_rn(val[u * mp + t], xv);
     }
 #pragma unroll
-    for (int u = 0; u < W; ++u) acc = sub_prod(acc, vv[u], xv[u]);
+    for (int u = 0; u < W; ++u) acc = __dsub_rn(acc, p[u]);
     return acc;
 }
 
-// Runtime width, any dependency kind (global x allowed); groups of 8 loads.
-__device__ __noinline__ double accumulate_generic(double acc, int w, const int* dep, const double* val, int mp, int t,
-                                                  const double* xs, const double* ring, int ring_n, int hoff) {
-    for (int k0 = 0; k0 < w; k0 += 8) {
-        double xv[8], vv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const bool on = k0 + u < w;
-            const int d = on ? dep[(k0 + u) * mp + t] : -(ring_n + 1);
-            vv[u] = on ? val[(k0 + u) * mp + t] : 0.0;
-            xv[u] = dep_value(d, xs, ring, ring_n, hoff);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (k0 + u < w) acc = sub_prod(acc, vv[u], xv[u]);
-    }
-    return acc;
-}
-
-__device__ __forceinline__ double accumulate(double acc, int w, bool global, const int* dep, const double* val,
-                                             int mp, int t, const double* xs, const double* ring, int ring_n,
-                                             int hoff) {
-    if (!global) {
-        switch (w) {
-#define HEC_W(N) \
-    case N: return accumulate_fixed<N>(acc, dep, val, mp, t, ring, ring_n, hoff);
-            case 0: return acc;
-            HEC_W(1) HEC_W(2) HEC_W(3) HEC_W(4) HEC_W(5) HEC_W(6) HEC_W(7) HEC_W(8)
-            HEC_W(9) HEC_W(10) HEC_W(11) HEC_W(12) HEC_W(13) HEC_W(14) HEC_W(15) HEC_W(16)
-#undef HEC_W
-            default: break;
-        }
-    }
-    return accumulate_generic(acc, w, dep, val, mp, t, xs, ring, ring_n, hoff);
-}
-
-template <int NSOLVE, bool TRACE>
-__global__ void __launch_bounds__(kPipelineRoleThreads + NSOLVE, 1) k_pipeline(PipeArgs a) {
+// Shared-memory control block (kWaveCtrlBytes): prog[32] | slot[32] {ready,
+// blob offset} | roff[32] | bar_full[32] | bar_empty[32] | bar_b[32] | boff[32]
+// | ticket. roff = region start (producer), boff = blob start (waiters).
+template <int W, int NW, bool TRACE>
+__global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs a) {
+    constexpr int kSeg = plan::kWaveHeaderBytes;
+    constexpr int kDiag = kSeg + 8 * NW;  // 16-byte multiple
     extern __shared__ __align__(128) unsigned char smem[];
-    const int NS = a.nslots;
-    uint64_t* bar_full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* bar_clear = bar_full + NS;
-    uint64_t* bar_empty = bar_clear + NS;
+    uint32_t* prog = reinterpret_cast<uint32_t*>(smem);
+    uint2* slot = reinterpret_cast<uint2*>(smem + 128);
+    uint32_t* roff = reinterpret_cast<uint32_t*>(smem + 384);
+    uint64_t* bar_full = reinterpret_cast<uint64_t*>(smem + 512);
+    uint64_t* bar_empty = bar_full + 32;
+    uint64_t* bar_b = bar_empty + 32;
+    uint32_t* boff = reinterpret_cast<uint32_t*>(smem + 1280);
+    int* s_cta = reinterpret_cast<int*>(smem + 1408);
     double* ring = reinterpret_cast<double*>(smem + a.ring_off);
-    unsigned char* slots = smem + a.slot_off;
-    __shared__ int s_cta;
+    unsigned char* buf = smem + a.buf_off;
+    const int NS = a.inflight, LG = a.inflight_log2;
+    const int R = a.ring;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
+    if (tid < 128) prog[tid] = 0u;  // prog, slot, roff
     if (tid == 0) {
-        s_cta = static_cast<int>(atomicAdd(&a.counters[0], 1u));
+        *s_cta = static_cast<int>(atomicAdd(&a.counters[0], 1u));
         for (int s = 0; s < NS; ++s) {
             mbar_init(&bar_full[s], 1);
-            // 32 producer lanes (b gather, cp.async arrive-on) + the waiter's arrive
-            mbar_init(&bar_clear[s], 33);
-            mbar_init(&bar_empty[s], 1);
+            mbar_init(&bar_empty[s], NW);
+            mbar_init(&bar_b[s], 32);  // one cp.async arrive-on per waiter lane
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        ring[a.ring] = 0.0;  // the zero slot that padding entries point at
+        ring[R] = 0.0;  // the slot padding entries point at
     }
     __syncthreads();
-    const int c = s_cta;
+    const int c = *s_cta;
     const int c0 = a.cta_chunk0[c];
     const int nch = a.cta_chunk0[c + 1] - c0;
-    // slot = [gathered b : b_bytes][staged halo : halo_bytes][blob]
-    auto slot_ptr = [&](int s) { return slots + static_cast<size_t>(s) * a.slot_bytes; };
-    const int blob_off = a.b_bytes + a.halo_bytes;
-    auto tr = [&](int j, int k) -> unsigned long long& { return a.trace[static_cast<size_t>(c0 + j) * 16 + k]; };
+    auto tr = [&](int j, int k) -> unsigned long long& { return a.trace[static_cast<size_t>(c0 + j) * 64 + k]; };
 
     if (warp == 0) {
-        // ---------------- producer: blob prefetch + b gather ----------------
-        const int lag = a.lag;
-        int2 span_reg = make_int2(0, 0);
-        for (int j = 0; j < nch + lag; ++j) {
-            if (j < nch) {
-                if ((j & 31) == 0) {
-                    const int g = j + lane;
-                    span_reg = g < nch ? a.spans[c0 + g] : make_int2(0, 0);
-                }
-                const int off16 = __shfl_sync(0xffffffffu, span_reg.x, j & 31);
-                const int bytes = __shfl_sync(0xffffffffu, span_reg.y, j & 31);
-                const int s = j % NS, use = j / NS;
-                if (use > 0) mbar_wait(&bar_empty[s], (use - 1) & 1);
-                if (lane == 0) {
-                    if (TRACE) tr(j, 0) = gtimer();
-                    mbar_expect_tx(&bar_full[s], static_cast<uint32_t>(bytes));
-                    bulk_g2s(slot_ptr(s) + blob_off, a.blobs + static_cast<size_t>(off16) * 16,
-                             static_cast<uint32_t>(bytes), &bar_full[s]);
-                }
-                __syncwarp();
+        // ------------- producer: byte-ring allocation + bulk copy of chunk blobs -------------
+        int head = 0, oldest = 0;
+        int4 sp_reg = make_int4(0, 0, 0, 0);
+        for (int j = 0; j < nch; ++j) {
+            if ((j & 31) == 0) {
+                const int g = j + lane;
+                sp_reg = g < nch ? a.spans[c0 + g] : make_int4(0, 0, 0, 0);
             }
-            const int g = j - lag;
-            if (g >= 0 && g < nch) {
-                const int s = g % NS, use = g / NS;
-                mbar_wait(&bar_full[s], use & 1);
-                unsigned char* sp = slot_ptr(s);
-                const ChunkHeader* h = reinterpret_cast<const ChunkHeader*>(sp + blob_off);
-                const int m = h->m;
-                const int* bidx = reinterpret_cast<const int*>(sp + blob_off + h->bidx);
-                double* bst = reinterpret_cast<double*>(sp);
-                if (TRACE && lane == 0) tr(g, 1) = gtimer();
-                for (int t = lane; t < m; t += 32) cp_async8(bst + t, a.b + bidx[t]);
-                cp_async_arrive(&bar_clear[s]);
+            const int off16 = __shfl_sync(0xffffffffu, sp_reg.x, j & 31);
+            const int bytes = __shfl_sync(0xffffffffu, sp_reg.y, j & 31);
+            const int need = __shfl_sync(0xffffffffu, sp_reg.z, j & 31);
+            const int bbytes = __shfl_sync(0xffffffffu, sp_reg.w, j & 31);
+            const int s = j & (NS - 1);
+            if (j >= NS) {
+                mbar_wait(&bar_empty[s], ((j >> LG) - 1) & 1);
+                oldest = max(oldest, j - NS + 1);
+            }
+            int pos;
+            for (;;) {
+                if (oldest == j) {  // nothing in flight: restart at the front
+                    pos = 0;
+                    break;
+                }
+                // live region starts at the oldest chunk's region (its b area)
+                const int tail = static_cast<int>(roff[oldest & (NS - 1)]);
+                if (head >= tail) {
+                    if (head + need <= a.buf_bytes) { pos = head; break; }
+                    if (need < tail) { pos = 0; break; }
+                } else if (head + need < tail) {
+                    pos = head;
+                    break;
+                }
+                mbar_wait(&bar_empty[oldest & (NS - 1)], (oldest >> LG) & 1);
+                ++oldest;
+            }
+            if (lane == 0) {
+                roff[s] = static_cast<uint32_t>(pos);
+                boff[s] = static_cast<uint32_t>(pos + bbytes);
+                if (TRACE) tr(j, 0) = gtimer();
+                mbar_expect_tx(&bar_full[s], static_cast<uint32_t>(bytes));
+                bulk_g2s(buf + pos + bbytes, a.blobs + static_cast<size_t>(off16) * 16, static_cast<uint32_t>(bytes),
+                         &bar_full[s]);
+            }
+            __syncwarp();
+            head = pos + need;
+        }
+    } else if (warp <= kWaveWaiters) {
+        // ------------- waiters (round robin over chunks): gather b (completion on
+        // bar_b), stage the foreign values, publish the chunk -------------
+        const uint32_t ep = a.epoch;
+        for (int j = warp - 1; j < nch; j += kWaveWaiters) {
+            const int s = j & (NS - 1);
+            mbar_wait(&bar_full[s], (j >> LG) & 1);
+            unsigned char* blob = buf + boff[s];  // region = [b: 8 mp][blob][staged halo]
+            const int4 hb0 = *reinterpret_cast<const int4*>(blob);       // m, mp, q0, flags
+            const int4 hb1 = *reinterpret_cast<const int4*>(blob + 16);  // nhalo, halo, tptr, bytes
+            if (TRACE && lane == 0) tr(j, 1) = gtimer();
+            const int m = hb0.x, mp = hb0.y;
+            const int* bidx = reinterpret_cast<const int*>(blob + kDiag + 8 * mp + 12 * W * mp);
+            double* bst = reinterpret_cast<double*>(blob - 8 * mp);
+            for (int t = lane; t < m; t += 32) cp_async8(bst + t, a.b + bidx[t]);
+            cp_async_arrive(&bar_b[s]);
+            const int nhalo = hb1.x;
+            if (nhalo) {
+                const int* hid = reinterpret_cast<const int*>(blob + hb1.y);
+                double* hst = reinterpret_cast<double*>(blob + hb1.w);
+                for (int t0 = 0; t0 < nhalo; t0 += 32 * 8) {
+                    ulonglong2 v[8];
+                    int id[8];
+                    unsigned miss = 0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {  // 8 loads in flight per lane
+                        const int t = t0 + u * 32 + lane;
+                        id[u] = t < nhalo ? hid[t] : -1;
+                        if (id[u] >= 0) {
+                            v[u] = ld_relaxed_v2(a.mbox + 2 * static_cast<size_t>(id[u]));
+                            miss |= 1u << u;
+                        }
+                    }
+                    // re-read every value not produced yet, all in flight, until complete
+                    for (;;) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if ((miss >> u) & 1u) {
+                                if (mail_ok(v[u], ep)) {
+                                    hst[t0 + u * 32 + lane] = mail_value(v[u]);
+                                    miss &= ~(1u << u);
+                                }
+                            }
+                        if (!__any_sync(0xffffffffu, miss != 0)) break;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if ((miss >> u) & 1u) v[u] = ld_relaxed_v2(a.mbox + 2 * static_cast<size_t>(id[u]));
+                    }
+                }
+            }
+            if (TRACE && lane == 0) tr(j, 2) = gtimer();
+            __syncwarp();
+            asm volatile("fence.acq_rel.cta;" ::: "memory");
+            if (lane == 0) {
+                st_volatile_v2(&slot[s], static_cast<uint32_t>(j + 1), static_cast<uint32_t>(blob - buf));
+                if (TRACE) tr(j, 3) = gtimer();
             }
         }
-    } else if (warp == 1) {
-        // ---------------- waiter: poll foreign values, stage them ----------------
+    } else {
+        // ------------- solvers: warp w owns a fixed slice of the CTA's rows -------------
+        const int w = warp - 1 - kWaveWaiters;
+        const uint32_t ep = a.epoch;
+        const uint32_t ring_s = smem_u32(ring);
+        const int L = a.lead;
+        double* const xs = a.xs;
+        double* const outv = a.out;
+        unsigned long long* const mbox = a.mbox;
         for (int j = 0; j < nch; ++j) {
-            const int s = j % NS, use = j / NS;
-            mbar_wait(&bar_full[s], use & 1);
-            unsigned char* sp = slot_ptr(s);
-            const unsigned char* blob = sp + blob_off;
-            const int nhalo = reinterpret_cast<const ChunkHeader*>(blob)->nhalo;
-            if (TRACE && lane == 0) tr(j, 2) = gtimer();
-            const int* hcode = reinterpret_cast<const int*>(blob + plan::kChunkHeaderBytes);
-            double* hst = reinterpret_cast<double*>(sp + a.b_bytes);
-            for (int t0 = 0; t0 < nhalo; t0 += 128) {
-                unsigned long long v[4];
-                int code[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {  // 4 polls in flight per lane
-                    const int t = t0 + u * 32 + lane;
-                    code[u] = t < nhalo ? hcode[t] : -1;
-                    v[u] = code[u] >= 0 ? ld_relaxed_u64(a.mbox + (code[u] >> 1)) : 0ULL;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (code[u] < 0) continue;
-                    unsigned long long* mb = a.mbox + (code[u] >> 1);
-                    while (v[u] == kEmpty) v[u] = ld_relaxed_u64(mb);
-                    hst[t0 + u * 32 + lane] = __longlong_as_double(static_cast<long long>(v[u]));
-                    if (code[u] & 1) st_relaxed_u64(mb, kEmpty);  // last use this solve: re-arm
+            const int s = j & (NS - 1);
+            uint2 si;
+            do {
+                si = ld_volatile_v2(&slot[s]);
+            } while (si.x != static_cast<uint32_t>(j + 1));
+            mbar_wait(&bar_b[s], (j >> LG) & 1);  // gathered b landed (normally long ago)
+            if (TRACE && lane == 0) tr(j, 8 + 3 * w) = gtimer();
+            const unsigned char* blob = buf + si.y;
+            const int4 h0 = *reinterpret_cast<const int4*>(blob);  // m, mp, q0, flags
+            const uint2 sg = *reinterpret_cast<const uint2*>(blob + kSeg + 8 * w);
+            const int t0 = static_cast<int>(sg.x & 0xffffu), t1 = static_cast<int>(sg.x >> 16);
+            // the warps this segment reads from must have finished chunk j-1, and every
+            // warp chunk j-lead (no warp runs further ahead: ring safety, tri_plan.hpp)
+            if (lane < NW) {
+                const uint32_t need = ((sg.y >> lane) & 1u) ? static_cast<uint32_t>(j)
+                                                            : static_cast<uint32_t>(max(0, j - L + 1));
+                while (ld_volatile_u32(&prog[lane]) < need) {
                 }
             }
             __syncwarp();
-            if (TRACE && lane == 0) tr(j, 3) = gtimer();
-            if (lane == 0) mbar_arrive(&bar_clear[s]);
-        }
-    } else {
-        // ---------------- solvers: one row per thread per pass ----------------
-        const int st = tid - kPipelineRoleThreads;
-        const int ring_mask = a.ring - 1;
-        const int ring_n = a.ring;
-        for (int j = 0; j < nch; ++j) {
-            const int s = j % NS, use = j / NS;
-            mbar_wait(&bar_clear[s], use & 1);
-            long long clk0 = 0;
-            if (TRACE && st == 0) {
-                tr(j, 4) = gtimer();
-                clk0 = clock64();
+            if (TRACE && lane == 0) tr(j, 9 + 3 * w) = gtimer();
+            if (t1 > t0) {
+                const int mp = h0.y, q0 = h0.z, flags = h0.w;
+                const double* dg = reinterpret_cast<const double*>(blob + kDiag);
+                const double* val = dg + mp;
+                const int* dep = reinterpret_cast<const int*>(val + W * mp);
+                const int* xidx = dep + (W + 1) * mp;
+                const int* exl = xidx + mp;
+                const double* bst = reinterpret_cast<const double*>(blob) - mp;
+                const double* hb = reinterpret_cast<const double*>(blob + reinterpret_cast<const int*>(blob)[7]) - (R + 1);
+                // one row per lane (the layout splits chunks so a warp never has more than 32)
+                const bool act = t0 + lane < t1;
+                const int t = act ? t0 + lane : t0;
+                const double dv = dg[t];
+                const int e = exl[t], xi = xidx[t];
+                double x;
+                if ((flags & 9) == 0) {
+                    // fast path: every dependency in shared memory, no tail
+                    int dd[W];
+                    double vv[W], xv[W];
+#pragma unroll
+                    for (int u = 0; u < W; ++u) {
+                        dd[u] = dep[u * mp + t];
+                        vv[u] = val[u * mp + t];
+                    }
+#pragma unroll
+                    for (int u = 0; u < W; ++u) xv[u] = (dd[u] <= R ? ring : hb)[dd[u]];
+                    const double y = __drcp_rn(dv);  // off the critical path
+                    double acc = bst[t];
+#pragma unroll
+                    for (int u = 0; u < W; ++u) acc = __dsub_rn(acc, __dmul_rn(vv[u], xv[u]));
+                    x = div_rn(acc, dv, y);
+                } else {
+                    const double y = __drcp_rn(dv);
+                    double acc = bst[t];
+                    const uint32_t ring_s = smem_u32(ring), hb_s = smem_u32(hb);
+#pragma unroll
+                    for (int u = 0; u < W; ++u)
+                        acc = __dsub_rn(acc, __dmul_rn(val[u * mp + t], dep_value(dep[u * mp + t], R, ring_s, hb_s, xs)));
+                    if (flags & 1) {  // CSR tail beyond the sliced-ELL width, storage order
+                        const int* tptr = reinterpret_cast<const int*>(blob + reinterpret_cast<const int*>(blob)[6]);
+                        const int mt = (mp + 4) & ~3;  // round_up(mp + 1, 4)
+                        const int ntl = tptr[mp];
+                        const double* tval = reinterpret_cast<const double*>(tptr + mt);
+                        const int* tdep = reinterpret_cast<const int*>(tval + ((ntl + 1) & ~1));
+                        for (int k = tptr[t]; k < tptr[t + 1]; ++k)
+                            acc = __dsub_rn(acc, __dmul_rn(tval[k], dep_value(tdep[k], R, ring_s, hb_s, xs)));
+                    }
+                    x = div_rn(acc, dv, y);
+                }
+                // consumers in other CTAs are on the critical path: feed them first
+                if (act && e >= 0) mail_store(mbox + 2 * static_cast<size_t>(e), x, ep);
+                if (act) {
+                    ring[(q0 + t) & (R - 1)] = x;
+                    xs[xi] = x;
+                    if (flags & 2) {
+                        const int o = exl[mp + t];
+                        if (o >= 0) outv[o] = x;
+                    }
+                }
             }
-            unsigned char* sp = slot_ptr(s);
-            const unsigned char* blob = sp + blob_off;
-            const ChunkHeader h = *reinterpret_cast<const ChunkHeader*>(blob);
-            const double* bst = reinterpret_cast<const double*>(sp);
-            // staged halo, addressed relative to the ring base (both in shared memory)
-            const int hoff =
-                static_cast<int>((sp + a.b_bytes - reinterpret_cast<unsigned char*>(ring)) / 8) - (ring_n + 1);
-            const bool global = (h.flags & 8) != 0;
-            if (TRACE && st == 0) tr(j, 8) = clock64() - clk0;
-            for (int t = st; t < h.m; t += NSOLVE) {
-                double acc = accumulate(bst[t], h.w, global, reinterpret_cast<const int*>(blob + h.dep),
-                                        reinterpret_cast<const double*>(blob + h.val), h.mp, t, a.xs, ring, ring_n,
-                                        hoff);
-                if (h.flags & 1) {
-                    const int* tptr = reinterpret_cast<const int*>(blob + h.tptr);
-                    const double* tval = reinterpret_cast<const double*>(blob + h.tval);
-                    const int* tdep = reinterpret_cast<const int*>(blob + h.tdep);
-                    for (int e = tptr[t]; e < tptr[t + 1]; ++e)
-                        acc = sub_prod(acc, tval[e], dep_value(tdep[e], a.xs, ring, ring_n, hoff));
-                }
-                if (TRACE && t == 0) {
-                    asm volatile("" ::"d"(acc) : "memory");
-                    tr(j, 9) = clock64() - clk0;
-                }
-                const double x = __ddiv_rn(acc, reinterpret_cast<const double*>(blob + h.diag)[t]);
-                if (TRACE && t == 0) {
-                    asm volatile("" ::"d"(x) : "memory");
-                    tr(j, 10) = clock64() - clk0;
-                }
-                if (h.flags & 4) {  // feed the consumers' mailboxes first: they are on the critical path
-                    const int* mbptr = reinterpret_cast<const int*>(blob + h.mbptr);
-                    const int* mbid = reinterpret_cast<const int*>(blob + h.mbid);
-                    const unsigned long long xb = static_cast<unsigned long long>(__double_as_longlong(x));
-                    for (int k = mbptr[t]; k < mbptr[t + 1]; ++k) st_relaxed_u64(a.mbox + mbid[k], xb);
-                }
-                ring[(h.q0 + t) & ring_mask] = x;
-                a.xs[reinterpret_cast<const int*>(blob + h.xidx)[t]] = x;
-                if (h.flags & 2) {
-                    const int o = reinterpret_cast<const int*>(blob + h.oidx)[t];
-                    if (o >= 0) a.out[o] = x;
-                }
+            __syncwarp();
+            asm volatile("fence.acq_rel.cta;" ::: "memory");
+            if (lane == 0) {
+                st_volatile_u32(&prog[w], static_cast<uint32_t>(j + 1));
+                mbar_arrive(&bar_empty[s]);
+                if (TRACE) tr(j, 10 + 3 * w) = gtimer();
             }
-            if (TRACE && st == 0) tr(j, 11) = clock64() - clk0;
-            named_bar_sync(1, NSOLVE);
-            if (TRACE && st == 0) {
-                tr(j, 5) = gtimer();
-                tr(j, 7) = static_cast<unsigned long long>(clock64() - clk0);
-            }
-            if (st == 0) mbar_arrive(&bar_empty[s]);
         }
     }
 
@@ -374,29 +476,24 @@ __global__ void __launch_bounds__(kPipelineRoleThreads + NSOLVE, 1) k_pipeline(P
     }
 }
 
-template __global__ void k_pipeline<128, false>(PipeArgs);
-template __global__ void k_pipeline<256, false>(PipeArgs);
-template __global__ void k_pipeline<128, true>(PipeArgs);
-template __global__ void k_pipeline<256, true>(PipeArgs);
+#define HEC_WAVE_INST(WD)                                    \
+    template __global__ void k_wave<WD, 16, false>(WaveArgs); \
+    template __global__ void k_wave<WD, 16, true>(WaveArgs);
+HEC_WAVE_INST(1) HEC_WAVE_INST(2) HEC_WAVE_INST(3) HEC_WAVE_INST(4) HEC_WAVE_INST(5) HEC_WAVE_INST(6)
+HEC_WAVE_INST(7) HEC_WAVE_INST(8) HEC_WAVE_INST(10) HEC_WAVE_INST(13) HEC_WAVE_INST(16)
+#undef HEC_WAVE_INST
 
-void* pipeline_kernel(int nsolve, bool trace) {
-    if (trace)
-        return nsolve >= 256 ? reinterpret_cast<void*>(&k_pipeline<256, true>)
-                             : reinterpret_cast<void*>(&k_pipeline<128, true>);
-    return nsolve >= 256 ? reinterpret_cast<void*>(&k_pipeline<256, false>)
-                         : reinterpret_cast<void*>(&k_pipeline<128, false>);
-}
-
-// Fill a mailbox array with the empty sentinel.
-__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        p[i] = v;
-}
-
-void fill_mailboxes(unsigned long long* p, long long n, cudaStream_t st) {
-    if (n <= 0) return;
-    k_fill_u64<<<296, 256, 0, st>>>(p, n, kEmpty);
+void* wave_kernel(int width, bool trace) {
+#define HEC_PICK(WD)                                                                   \
+    case WD:                                                                           \
+        return trace ? reinterpret_cast<void*>(&k_wave<WD, kWaveSolverWarps, true>)  \
+                     : reinterpret_cast<void*>(&k_wave<WD, kWaveSolverWarps, false>);
+    switch (width) {
+        HEC_PICK(1) HEC_PICK(2) HEC_PICK(3) HEC_PICK(4) HEC_PICK(5) HEC_PICK(6)
+        HEC_PICK(7) HEC_PICK(8) HEC_PICK(10) HEC_PICK(13) HEC_PICK(16)
+        default: return nullptr;
+    }
+#undef HEC_PICK
 }
 
 }  // namespace hec::dev

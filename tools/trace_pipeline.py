@@ -45,65 +45,77 @@ def main():
     torch.cuda.synchronize()
     tr, c0 = t.solve_traced(b, x)
     tr = tr.astype(np.int64)
+    nw = info["threads"] // 32 - 4  # producer + 3 waiter warps
     t0 = tr[:, 0].min()
-    T = tr - t0
-    T[:, 7] = tr[:, 7]
-    end = T[:, 5].max()
-    print(f"chunks {len(T)}  span {end/1e3:.1f} us (first blob issue -> last publish)")
-    names = ["issue", "gather", "wstart", "cleared", "sstart", "sdone", "publish"]
-    print("blob issue -> gather issue (ns):   ", q(T[:, 1] - T[:, 0]))
-    print("gather -> waiter start:            ", q(T[:, 2] - T[:, 1]))
-    print("waiter poll (start -> cleared):    ", q(T[:, 3] - T[:, 2]))
-    print("cleared -> solvers start:          ", q(T[:, 4] - T[:, 3]))
-    print("solvers compute (start -> done):   ", q(T[:, 5] - T[:, 4]))
-    print("solver SM cycles:                  ", q(T[:, 7]))
-    print("  cycles to header decoded:        ", q(tr[:, 8]))
-    print("  cycles to acc (row 0):           ", q(tr[:, 9]))
-    print("  cycles to x (after div):         ", q(tr[:, 10]))
-    print("  cycles to rows done (thread 0):  ", q(tr[:, 11]))
-    # solver idle gap between consecutive chunks of one CTA
-    gaps, busy, first_start, last_done = [], [], [], []
-    for c in range(len(c0) - 1):
+    T = np.where(tr > 0, tr - t0, -1)
+    rs = T[:, 8:8 + 3 * nw:3]     # ready seen per warp
+    dd = T[:, 9:9 + 3 * nw:3]     # deps satisfied (only for non-empty segments)
+    dn = T[:, 10:10 + 3 * nw:3]   # done per warp
+    last = dn.max(axis=1)
+    print(f"chunks {len(T)}  span {last.max()/1e3:.1f} us  solver warps {nw}")
+    print("blob issue -> waiter sees blob (ns): ", q(T[:, 1] - T[:, 0]))
+    print("waiter: blob -> halo staged:         ", q(T[:, 2] - T[:, 1]))
+    print("waiter: halo -> ready:               ", q(T[:, 3] - T[:, 2]))
+    busy = dd >= 0
+    print("ready -> warp sees ready:            ", q((rs - T[:, 3:4])[busy]))
+    print("warp sees ready -> deps satisfied:   ", q((dd - rs)[busy]))
+    print("deps satisfied -> warp done:         ", q((dn - dd)[busy]))
+    print("first warp ready-seen -> last done:  ", q(last - rs.min(axis=1)))
+    for k, nm in enumerate(["drcp issued+diag", "accumulated", "divided", "stored"]):
+        v = tr[:, 56 + k]
+        print(f"   even-warp cycles to {nm:18s}", q(v[v > 0]))
+    # per warp: how long after the previous chunk's done does it see ready
+    for c in [0, 1, 70, len(c0) - 2]:
         lo, hi = c0[c], c0[c + 1]
-        if hi <= lo:
+        if hi - lo < 3:
             continue
-        st, dn = T[lo:hi, 4], T[lo:hi, 5]
-        gaps.extend((st[1:] - dn[:-1]).tolist())
-        busy.append((dn - st).sum())
-        first_start.append(st[0])
-        last_done.append(dn[-1])
-    print("solver gap between chunks (ns):    ", q(gaps))
-    busy = np.array(busy)
-    span = np.array(last_done) - np.array(first_start)
-    print(f"per-CTA busy fraction: mean {np.mean(busy / np.maximum(span, 1)):.3f}; "
-          f"first start p50 {np.median(first_start)/1e3:.1f} us, last done p50 {np.median(last_done)/1e3:.1f} us")
-    # where does the gap go: waiting for the waiter (cross-CTA) or for data (producer)?
-    wait_cross = T[:, 3] - np.maximum(T[:, 2], 0)
-    print("gap attributable to cross-CTA wait (cleared - wstart) when solvers idle:")
-    idle_cross, idle_data = [], []
-    for c in range(len(c0) - 1):
-        lo, hi = c0[c], c0[c + 1]
-        for j in range(lo + 1, hi):
-            gap_start = T[j - 1, 5]
-            if T[j, 4] - gap_start < 200:
+        per = np.diff(last[lo:hi])
+        print(f"CTA {c}: chunks {hi-lo} first {rs[lo].min()/1e3:.1f} us last {last[hi-1]/1e3:.1f} us "
+              f"period p50 {np.median(per):.0f} ns mean {per.mean():.0f} ns")
+        # warp-level gaps: for each warp, idle time between done(j-1) and deps-satisfied(j)
+        for w in range(nw):
+            m = busy[lo:hi, w]
+            if m.sum() < 3:
                 continue
-            # data ready at T[j,2] (waiter saw full+ready), cross cleared at T[j,3]
-            idle_data.append(max(0, T[j, 2] - gap_start))
-            idle_cross.append(max(0, T[j, 3] - max(T[j, 2], gap_start)))
-    print("   data (producer) part:   ", q(idle_data))
-    print("   cross-CTA wait part:    ", q(idle_cross))
-    # per-CTA detail (ticket order == owner order)
-    print("cta  chunks  first_start  last_done  us/chunk  busy%  mean_gap  wstart->cleared  cleared->start")
-    for c in sorted(set([0, 1, 2, 3, 5, 10, 30, 70, 110, len(c0) - 2])):
-        lo, hi = c0[c], c0[c + 1]
-        if hi <= lo:
-            continue
-        st, dn = T[lo:hi, 4], T[lo:hi, 5]
-        span = dn[-1] - st[0]
-        busy = (dn - st).sum()
-        print(f"{c:4d} {hi-lo:6d} {st[0]/1e3:11.1f} {dn[-1]/1e3:10.1f} {span/(hi-lo)/1e3:9.2f} {100*busy/max(span,1):6.1f} "
-              f"{np.mean(st[1:]-dn[:-1]) if hi-lo>1 else 0:9.0f} {np.median(T[lo:hi,3]-T[lo:hi,2]):15.0f} "
-              f"{np.median(T[lo:hi,4]-T[lo:hi,3]):14.0f}")
+            wait_ready = (rs[lo + 1:hi, w] - dn[lo:hi - 1, w])
+            wait_deps = (dd[lo:hi, w] - rs[lo:hi, w])[m]
+            work = (dn[lo:hi, w] - dd[lo:hi, w])[m]
+            print(f"   warp {w:2d} busy chunks {m.sum():4d}  wait-ready p50 {np.median(wait_ready):6.0f}  "
+                  f"wait-deps p50 {np.median(wait_deps):6.0f}  work p50 {np.median(work):6.0f}  ns")
+    # raw timeline of a few consecutive chunks (ns, relative to the first issue)
+    for c in [0, 70]:
+        lo = c0[c]
+        print(f"CTA {c} chunks 200..205: issue / waiter-sees / halo / ready ; per warp ready-seen,deps,done (-1 = empty)")
+        for j in range(lo + 200, min(lo + 206, c0[c + 1])):
+            print(f"  j={j-lo}: {T[j,0]} / {T[j,1]} / {T[j,2]} / {T[j,3]} ;",
+                  " ".join(f"w{w}:{rs[j,w]},{dd[j,w]},{dn[j,w]}" for w in range(nw)))
+    # handoff analysis: chunk (c, level L) vs producer chunk (c-1, level L-1)
+    ls = np.asarray(p.schedule.level_starts)
+    ip = np.asarray(p.schedule.inv_perm)
+    C = len(c0) - 1
+    per = (p.n + C - 1) // C
+    own = np.minimum(ip // per, C - 1)
+    lev_of_r = np.repeat(np.arange(len(ls) - 1), np.diff(ls))
+    key = np.unique(own.astype(np.int64) * 100000 + lev_of_r)
+    kc, kl = key // 100000, key % 100000
+    if len(key) == len(T):
+        idx = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(kc, kl))}
+        lat, slack = [], []
+        for i in range(len(T)):
+            src = idx.get((int(kc[i]) - 1, int(kl[i]) - 1))
+            if src is None or T[i, 2] < 0:
+                continue
+            lat.append(T[i, 2] - last[src])       # halo complete - producer chunk done
+            slack.append(T[i, 1] - last[src])     # waiter saw blob - producer done (<0: waiter was waiting)
+        lat, slack = np.array(lat), np.array(slack)
+        print("halo staged - producer chunk done (ns):", q(lat))
+        print("waiter sees blob - producer done (ns): ", q(slack))
+        w_wait = lat[slack < 0]
+        print("  when the waiter was already polling:  ", q(w_wait))
+    else:
+        print("chunk keys", len(key), "!= chunks", len(T), "(split chunks): handoff analysis skipped")
+    starts = np.array([rs[c0[c]].min() for c in range(len(c0) - 1) if c0[c + 1] > c0[c]])
+    print("CTA first-chunk start offsets (us): p50 step %.3f" % (np.median(np.diff(starts)) / 1e3))
 
 
 if __name__ == "__main__":
