@@ -97,6 +97,16 @@ int hec_tri_create(int n, int reversal_applied, int nlev, const int* level_start
  */
 int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream);
 
+/*
+ * hec_tri_solve split in its two device passes, for pipelines that keep the
+ * right-hand side in the solve's reordered-row order (e.g. an operator that
+ * writes it there directly): bp[r] = b[input index of reordered row r]
+ * (the reference's permute-in, proj/src/triangular.cpp:110-111), then the
+ * solve from bp. bp must hold n + 2 doubles.
+ */
+int hec_tri_permute_in(hec_tri_t t, const double* b_dev, double* bp_dev, void* stream);
+int hec_tri_solve_ordered(hec_tri_t t, const double* bp_dev, double* x_dev, void* stream);
+
 /* Same with host vectors (H2D, solve, D2H; synchronous). Drop-in for hec::solve. */
 int hec_tri_solve_host(hec_tri_t t, const double* b, double* x);
 

@@ -329,6 +329,16 @@ class DeviceTri:
         check(lib.hec_tri_solve(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(x_dev)),
                                 C.c_void_p(_stream(stream)) if stream is not None else None))
 
+    def permute_in(self, b_dev, bp_dev, stream=None) -> None:
+        """bp[r] = b[input index of reordered row r]; bp holds n + 2 doubles."""
+        check(lib.hec_tri_permute_in(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(bp_dev)),
+                                     C.c_void_p(_stream(stream)) if stream is not None else None))
+
+    def solve_ordered(self, bp_dev, x_dev, stream=None) -> None:
+        """The solve from a right-hand side already in reordered-row order."""
+        check(lib.hec_tri_solve_ordered(self._h, C.c_void_p(_ptr(bp_dev)), C.c_void_p(_ptr(x_dev)),
+                                        C.c_void_p(_stream(stream)) if stream is not None else None))
+
     def solve_host(self, b) -> np.ndarray:
         bv = _f64_vec(b, None, "solve")
         x = np.empty_like(bv)

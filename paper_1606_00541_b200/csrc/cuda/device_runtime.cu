@@ -98,6 +98,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_exports_ = P.exports;
             p_blob_.upload(P.blob);
             p_spans_.upload(P.span);
+            p_bidx_.upload(P.bidx);
             p_cta0_.upload(P.cta_chunk0);
             p_cta0_host_ = P.cta_chunk0;
             stats_.ctas = p_ctas_;
@@ -105,7 +106,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
             stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size() +
-                                                         16 * P.exports);
+                                                         4 * P.bidx.size() + 16 * P.exports);
         } else {
             strategy_ = 1;  // a chunk too large for shared memory: level launches
         }
@@ -139,7 +140,7 @@ DeviceTri::~DeviceTri() {
 
 int DeviceTri::launches_per_solve() const {
     if (n_ == 0) return 0;
-    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 1;
+    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 2;  // permute-in + wave
 }
 
 DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
@@ -150,17 +151,35 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
         w->counters.alloc(2);
         HEC_CUDA(cudaMemset(w->counters.p, 0, sizeof(uint32_t) * 2));
         w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
+        w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
         HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
         HEC_CUDA(cudaDeviceSynchronize());
     }
     return *w;
 }
 
+void DeviceTri::permute(const double* b, double* bp, cudaStream_t st) const {
+    if (n_ == 0) return;
+    permute_in(b, strategy_ == 1 ? l_bidx_.p : p_bidx_.p, bp, n_, st);
+    HEC_CUDA(cudaGetLastError());
+}
+
 void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st, unsigned long long* trace) {
     if (n_ == 0) return;
     if (strategy_ == 1) {
+        run_levels(b, false, xs, out, st);  // the level kernels gather b themselves
+        return;
+    }
+    Workspace& w = workspace(st);
+    permute(b, w.bp.p, st);
+    solve_ordered(w.bp.p, xs, out, st, trace);
+}
+
+void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st) {
+    {
         LevelArgs a{};
         a.b = b;
+        a.b_ordered = ordered ? 1 : 0;
         a.xs = xs;
         a.out = has_out_ ? out : nullptr;
         a.bidx = l_bidx_.p;
@@ -176,6 +195,13 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st,
         a.ld = l_ld_;
         launch_levels(a, level_starts_.data(), static_cast<int>(level_starts_.size()) - 1, st);
         HEC_CUDA(cudaGetLastError());
+    }
+}
+
+void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStream_t st, unsigned long long* trace) {
+    if (n_ == 0) return;
+    if (strategy_ == 1) {
+        run_levels(bp, true, xs, out, st);
         return;
     }
     Workspace& w = workspace(st);
@@ -187,7 +213,7 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st,
     a.blobs = p_blob_.p;
     a.spans = reinterpret_cast<const int4*>(p_spans_.p);
     a.cta_chunk0 = p_cta0_.p;
-    a.b = b;
+    a.bp = bp;
     a.xs = xs;
     a.out = has_out_ ? out : nullptr;
     a.mbox = w.mailbox.p;

@@ -80,6 +80,11 @@ public:
     // xs[o] = solution; out[oidx] = solution where oidx >= 0 (if out != null).
     void solve(const double* b, double* xs, double* out, cudaStream_t st,
                unsigned long long* trace = nullptr);
+    // The two halves of solve(): bp[r] = b[bidx[r]] (bp holds n + 2 doubles), then
+    // the solve from the reordered right-hand side.
+    void permute(const double* b, double* bp, cudaStream_t st) const;
+    void solve_ordered(const double* bp, double* xs, double* out, cudaStream_t st,
+                       unsigned long long* trace = nullptr);
     // chunk -> CTA map of the pipeline layout (empty for LEVELS)
     const std::vector<int>& cta_chunk0() const { return p_cta0_host_; }
     // Synchronous host-vector convenience (pinned or pageable).
@@ -92,9 +97,11 @@ private:
     struct Workspace {
         DevBuf<uint32_t> counters;            // ticket + finished CTAs
         DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
+        DevBuf<double> bp;                    // right-hand side in reordered-row order
         uint32_t epoch = 0;                   // last solve's epoch on this stream
     };
     Workspace& workspace(cudaStream_t st);
+    void run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st);
 
     int n_ = 0;
     int strategy_ = 2;
@@ -107,7 +114,7 @@ private:
     bool has_out_ = false;
     // WAVE (persistent wavefront kernel)
     DevBuf<unsigned char> p_blob_;
-    DevBuf<int> p_spans_, p_cta0_;
+    DevBuf<int> p_spans_, p_cta0_, p_bidx_;
     int p_ctas_ = 0, p_inflight_ = 0, p_ring_ = 0, p_ring_off_ = 0, p_buf_off_ = 0, p_buf_bytes_ = 0;
     int p_smem_ = 0, p_warps_ = 0, p_lead_ = 1;
     void* p_kernel_ = nullptr;

@@ -22,13 +22,15 @@ struct LevelArgs {
     const double* tail_val;
     int width;
     int ld;
+    int b_ordered;          // b already in reordered-row order (bidx ignored)
 };
 
 struct WaveArgs {
     const unsigned char* blobs;  // all chunk blobs (16-byte aligned)
-    const int4* spans;           // per chunk: (blob offset / 16, blob bytes, region bytes, 0)
+    const int4* spans;           // 2 per chunk: (blob offset / 16, blob bytes, region bytes, r0),
+                                 //              (b area bytes, b copy bytes, 0, 0)
     const int* cta_chunk0;       // ctas + 1
-    const double* b;
+    const double* bp;            // right-hand side in reordered-row order
     double* xs;
     double* out;
     unsigned long long* mbox;    // 2 words per exported row: {lo32|epoch<<32, hi32|epoch<<32}
@@ -48,6 +50,8 @@ struct WaveArgs {
 void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
 // kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise)
 void* wave_kernel(int width, bool trace);
+// bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
+void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
 constexpr int kWaveWaiters = 3;                        // waiter warps
 constexpr int kWaveRoleThreads = 32 * (1 + kWaveWaiters);  // producer warp + waiter warps

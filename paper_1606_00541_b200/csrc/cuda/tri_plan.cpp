@@ -241,6 +241,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     P.chunks = P.cta_chunk0[C];
 
+    // input index of every reordered row (the permute-in pass before the solve)
+    P.bidx.resize(n);
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < n; ++r) {
+        const int o = sol_index(s, r);
+        P.bidx[r] = s.b_map ? s.b_map[o] : o;
+    }
+
     // 3. exports: rows read by another CTA get a mailbox id
     std::vector<int> export_id(n, -1);
     {
@@ -268,7 +276,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     for (int c = 0; c < C; ++c) {
         const auto& L = per_cta[c];
         auto& out = cta_blob[c];
-        cta_span[c].resize(4 * L.size());
+        cta_span[c].assign(8 * L.size(), 0);
         std::unordered_map<int, int> halo_of;
         std::vector<int> halo, dep, tptr, tdep;
         std::vector<double> val, tval;
@@ -338,7 +346,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             const int ntail = static_cast<int>(tdep.size());
             st_hval[c] += nhalo;
             (void)any_exp;  // the export list is always present (-1 = row not exported)
-            const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0);
+            const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0) |
+                              ((ch.r0 & 1) ? 32 : 0);
             const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
             const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
@@ -358,14 +367,12 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 const int r = ch.r0 + t;
                 const int o = sol_index(s, r);
                 put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
-                put_i(sec.bidx, t, s.b_map ? s.b_map[o] : o);
                 put_i(sec.xidx, t, o);
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
                 put_i(sec.exp, t, export_id[r]);
             }
             for (int t = m; t < mp; ++t) {  // padded rows: harmless values
                 put_d(sec.diag, t, 1.0);
-                put_i(sec.bidx, t, 0);
                 put_i(sec.exp, t, -1);
             }
             std::memcpy(b + sec.val, val.data(), 8 * val.size());
@@ -376,10 +383,13 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 std::memcpy(b + sec.tdep, tdep.data(), 4 * tdep.size());
             }
             region_max[c] = std::max(region_max[c], region);
-            cta_span[c][4 * j + 0] = static_cast<int>(base / 16);  // CTA-relative for now
-            cta_span[c][4 * j + 1] = round_up(sec.end, 16);
-            cta_span[c][4 * j + 2] = region;
-            cta_span[c][4 * j + 3] = 8 * mp;
+            int* sp = &cta_span[c][8 * j];
+            sp[0] = static_cast<int>(base / 16);  // CTA-relative for now
+            sp[1] = round_up(sec.end, 16);
+            sp[2] = region;
+            sp[3] = ch.r0;
+            sp[4] = wave_b_area(m);
+            sp[5] = round_up(8 * (m + (ch.r0 & 1)), 16);
         }
     }
     for (int c = 0; c < C; ++c)
@@ -394,16 +404,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     if (total / 16 > 0x7fffffffULL) throw std::overflow_error("hec_tri_create: layout exceeds 32 GiB");
     P.blob.resize(total);
-    P.span.assign(4 * static_cast<std::size_t>(P.chunks), 0);
+    P.span.assign(8 * static_cast<std::size_t>(P.chunks), 0);
     for (int c = 0; c < C; ++c) {
         std::memcpy(P.blob.data() + cta_base[c], cta_blob[c].data(), cta_blob[c].size());
         std::vector<unsigned char>().swap(cta_blob[c]);
         for (int j = 0; j < P.cta_chunk0[c + 1] - P.cta_chunk0[c]; ++j) {
             const int g = P.cta_chunk0[c] + j;
-            P.span[4 * g + 0] = cta_span[c][4 * j] + static_cast<int>(cta_base[c] / 16);
-            P.span[4 * g + 1] = cta_span[c][4 * j + 1];
-            P.span[4 * g + 2] = cta_span[c][4 * j + 2];
-            P.span[4 * g + 3] = cta_span[c][4 * j + 3];
+            for (int k = 0; k < 8; ++k) P.span[8 * g + k] = cta_span[c][8 * j + k];
+            P.span[8 * g] += static_cast<int>(cta_base[c] / 16);
         }
         P.max_region = std::max(P.max_region, region_max[c]);
         P.ring_deps += st_ring[c];

@@ -86,11 +86,16 @@ LevelLayout build_levels(const TriSource& s);
 //   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep R)
 //   int    dep[W][mp]    0 <= d < R: ring slot; d == R: 0.0 (padding);
 //                        d > R: staged halo value d-R-1; d < 0: x[-d-1]
-//   int bidx[mp], xidx[mp], exp[mp] (mailbox id or -1), (oidx[mp] if flags&2)
+//   int xidx[mp], exp[mp] (mailbox id or -1), (oidx[mp] if flags&2)
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
 //   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages
-// The shared-memory region of a chunk is [b: 8*mp][blob][staged halo: 8*nhalo];
-// the kernel addresses it from the blob start (b at -8*mp, halo at +bytes).
+// The right-hand side arrives permuted into reordered-row order (bp[r] =
+// b[bidx[r]], one coalesced pass before the solve), so a chunk's b values are
+// one contiguous range that a second bulk copy moves next to the blob. The
+// shared-memory region of a chunk is [b: 8*mb][blob][staged halo: 8*nhalo],
+// mb = round_up(m + 1, 4); b starts one element in when r0 is odd (flags&32,
+// the copy source is rounded down to 16 bytes). The kernel addresses the region
+// from the blob start (b at -8*mb, staged halo at +bytes).
 struct WaveConfig {
     int ctas = 148;
     int warps = 8;            // solver warps per CTA (<= 32)
@@ -110,19 +115,21 @@ struct WaveLayout {
     long long exports = 0;                // mailboxes
     bool has_out = false;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
-    std::vector<int> span;                // 4 per chunk: blob offset / 16, blob bytes, region bytes, b bytes
+    std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region bytes, r0,
+                                          //              b area bytes, b copy bytes, 0, 0
+    std::vector<int> bidx;                // n: input index of reordered row r (bp[r] = b[bidx[r]])
     std::vector<unsigned char> blob;      // all chunk blobs, 16-byte aligned
     long long ring_deps = 0, global_deps = 0, halo_deps = 0, halo_values = 0;
 };
 WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg);
 
 struct WaveSections {
-    int seg, diag, val, dep, bidx, xidx, exp, oidx, tptr, tval, tdep, halo, end;
+    int seg, diag, val, dep, xidx, exp, oidx, tptr, tval, tdep, halo, end;
 };
 
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
-    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo
+    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0
     int nhalo, halo, tptr, bytes;  // halo id list / tail offsets, blob bytes (= staged halo offset)
 };
 static_assert(sizeof(WaveHeader) == 32, "wave header is two 16-byte words");
@@ -138,7 +145,6 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     b.diag = at;  at += 8 * mp;
     b.val = at;   at += 8 * mp * w;
     b.dep = at;   at += 4 * mp * w;
-    b.bidx = at;  at += 4 * mp;
     b.xidx = at;  at += 4 * mp;
     b.exp = at;   at += 4 * mp;
     b.oidx = at;  if (flags & 2) at += 4 * mp;
@@ -149,9 +155,10 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     b.end = at;
     return b;
 }
-// shared-memory bytes of a chunk region: gathered b + blob + staged halo
+inline int wave_b_area(int m) { return 8 * round_up(m + 1, 4); }
+// shared-memory bytes of a chunk region: b + blob + staged halo
 inline int wave_region_bytes(int m, int nhalo, int blob_bytes) {
-    return 8 * round_up(m, 4) + round_up(blob_bytes, 16) + round_up(8 * nhalo, 16);
+    return wave_b_area(m) + round_up(blob_bytes, 16) + round_up(8 * nhalo, 16);
 }
 
 }  // namespace hec::plan

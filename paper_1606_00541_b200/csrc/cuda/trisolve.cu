@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "tri_kernels.cuh"
@@ -99,7 +100,7 @@ __device__ __forceinline__ double sub_prod(double acc, double v, double x) {
 __global__ void k_level_rows(LevelArgs a, int r0, int r1) {
     const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= r1) return;
-    double acc = a.b[a.bidx[r]];
+    double acc = a.b[a.b_ordered ? r : a.bidx[r]];
     for (int k = 0; k < a.width; ++k) {
         const size_t slot = static_cast<size_t>(k) * a.ld + r;
         const int d = a.ell_dep[slot];
@@ -217,20 +218,19 @@ __device__ __forceinline__ double accumulate(double acc, const int* dep, const d
     return acc;
 }
 
-// Shared-memory control block (kWaveCtrlBytes): prog[32] | slot[32] {ready,
-// blob offset} | roff[32] | bar_full[32] | bar_empty[32] | bar_b[32] | boff[32]
-// | ticket. roff = region start (producer), boff = blob start (waiters).
+// Shared-memory control block (kWaveCtrlBytes): prog[32] | hready[32] (+pad)
+// | roff[32] | bar_full[32] | bar_empty[32] | (unused) | boff[32] | ticket.
+// roff = region start (producer), boff = blob start.
 template <int W, int NW, bool TRACE>
 __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs a) {
     constexpr int kSeg = plan::kWaveHeaderBytes;
     constexpr int kDiag = kSeg + 8 * NW;  // 16-byte multiple
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t* prog = reinterpret_cast<uint32_t*>(smem);
-    uint2* slot = reinterpret_cast<uint2*>(smem + 128);
+    uint32_t* hready = reinterpret_cast<uint32_t*>(smem + 128);
     uint32_t* roff = reinterpret_cast<uint32_t*>(smem + 384);
     uint64_t* bar_full = reinterpret_cast<uint64_t*>(smem + 512);
     uint64_t* bar_empty = bar_full + 32;
-    uint64_t* bar_b = bar_empty + 32;
     uint32_t* boff = reinterpret_cast<uint32_t*>(smem + 1280);
     int* s_cta = reinterpret_cast<int*>(smem + 1408);
     double* ring = reinterpret_cast<double*>(smem + a.ring_off);
@@ -246,7 +246,6 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
         for (int s = 0; s < NS; ++s) {
             mbar_init(&bar_full[s], 1);
             mbar_init(&bar_empty[s], NW);
-            mbar_init(&bar_b[s], 32);  // one cp.async arrive-on per waiter lane
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         ring[R] = 0.0;  // the slot padding entries point at
@@ -260,16 +259,19 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
     if (warp == 0) {
         // ------------- producer: byte-ring allocation + bulk copy of chunk blobs -------------
         int head = 0, oldest = 0;
-        int4 sp_reg = make_int4(0, 0, 0, 0);
+        int4 sp_a = make_int4(0, 0, 0, 0), sp_b = make_int4(0, 0, 0, 0);
         for (int j = 0; j < nch; ++j) {
             if ((j & 31) == 0) {
                 const int g = j + lane;
-                sp_reg = g < nch ? a.spans[c0 + g] : make_int4(0, 0, 0, 0);
+                sp_a = g < nch ? a.spans[2 * (c0 + g)] : make_int4(0, 0, 0, 0);
+                sp_b = g < nch ? a.spans[2 * (c0 + g) + 1] : make_int4(0, 0, 0, 0);
             }
-            const int off16 = __shfl_sync(0xffffffffu, sp_reg.x, j & 31);
-            const int bytes = __shfl_sync(0xffffffffu, sp_reg.y, j & 31);
-            const int need = __shfl_sync(0xffffffffu, sp_reg.z, j & 31);
-            const int bbytes = __shfl_sync(0xffffffffu, sp_reg.w, j & 31);
+            const int off16 = __shfl_sync(0xffffffffu, sp_a.x, j & 31);
+            const int bytes = __shfl_sync(0xffffffffu, sp_a.y, j & 31);
+            const int need = __shfl_sync(0xffffffffu, sp_a.z, j & 31);
+            const int r0 = __shfl_sync(0xffffffffu, sp_a.w, j & 31);
+            const int bbytes = __shfl_sync(0xffffffffu, sp_b.x, j & 31);
+            const int bcopy = __shfl_sync(0xffffffffu, sp_b.y, j & 31);
             const int s = j & (NS - 1);
             if (j >= NS) {
                 mbar_wait(&bar_empty[s], ((j >> LG) - 1) & 1);
@@ -297,29 +299,24 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 roff[s] = static_cast<uint32_t>(pos);
                 boff[s] = static_cast<uint32_t>(pos + bbytes);
                 if (TRACE) tr(j, 0) = gtimer();
-                mbar_expect_tx(&bar_full[s], static_cast<uint32_t>(bytes));
+                mbar_expect_tx(&bar_full[s], static_cast<uint32_t>(bytes + bcopy));
                 bulk_g2s(buf + pos + bbytes, a.blobs + static_cast<size_t>(off16) * 16, static_cast<uint32_t>(bytes),
                          &bar_full[s]);
+                bulk_g2s(buf + pos, a.bp + (r0 & ~1), static_cast<uint32_t>(bcopy), &bar_full[s]);
             }
             __syncwarp();
             head = pos + need;
         }
     } else if (warp <= kWaveWaiters) {
-        // ------------- waiters (round robin over chunks): gather b (completion on
-        // bar_b), stage the foreign values, publish the chunk -------------
+        // ------------- waiters (round robin over chunks): stage the values this
+        // chunk reads from lower CTAs, then publish it -------------
         const uint32_t ep = a.epoch;
         for (int j = warp - 1; j < nch; j += kWaveWaiters) {
             const int s = j & (NS - 1);
             mbar_wait(&bar_full[s], (j >> LG) & 1);
-            unsigned char* blob = buf + boff[s];  // region = [b: 8 mp][blob][staged halo]
-            const int4 hb0 = *reinterpret_cast<const int4*>(blob);       // m, mp, q0, flags
+            unsigned char* blob = buf + boff[s];  // region = [b][blob][staged halo]
             const int4 hb1 = *reinterpret_cast<const int4*>(blob + 16);  // nhalo, halo, tptr, bytes
             if (TRACE && lane == 0) tr(j, 1) = gtimer();
-            const int m = hb0.x, mp = hb0.y;
-            const int* bidx = reinterpret_cast<const int*>(blob + kDiag + 8 * mp + 12 * W * mp);
-            double* bst = reinterpret_cast<double*>(blob - 8 * mp);
-            for (int t = lane; t < m; t += 32) cp_async8(bst + t, a.b + bidx[t]);
-            cp_async_arrive(&bar_b[s]);
             const int nhalo = hb1.x;
             if (nhalo) {
                 const int* hid = reinterpret_cast<const int*>(blob + hb1.y);
@@ -358,7 +355,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
             __syncwarp();
             asm volatile("fence.acq_rel.cta;" ::: "memory");
             if (lane == 0) {
-                st_volatile_v2(&slot[s], static_cast<uint32_t>(j + 1), static_cast<uint32_t>(blob - buf));
+                st_volatile_u32(&hready[s], static_cast<uint32_t>(j + 1));
                 if (TRACE) tr(j, 3) = gtimer();
             }
         }
@@ -373,16 +370,15 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
         unsigned long long* const mbox = a.mbox;
         for (int j = 0; j < nch; ++j) {
             const int s = j & (NS - 1);
-            uint2 si;
-            do {
-                si = ld_volatile_v2(&slot[s]);
-            } while (si.x != static_cast<uint32_t>(j + 1));
-            mbar_wait(&bar_b[s], (j >> LG) & 1);  // gathered b landed (normally long ago)
+            mbar_wait(&bar_full[s], (j >> LG) & 1);  // blob and b landed
             if (TRACE && lane == 0) tr(j, 8 + 3 * w) = gtimer();
-            const unsigned char* blob = buf + si.y;
+            const unsigned char* blob = buf + boff[s];
             const int4 h0 = *reinterpret_cast<const int4*>(blob);  // m, mp, q0, flags
             const uint2 sg = *reinterpret_cast<const uint2*>(blob + kSeg + 8 * w);
             const int t0 = static_cast<int>(sg.x & 0xffffu), t1 = static_cast<int>(sg.x >> 16);
+            if (h0.w & 16)  // values from lower CTAs staged by the waiters
+                while (ld_volatile_u32(&hready[s]) != static_cast<uint32_t>(j + 1)) {
+                }
             // the warps this segment reads from must have finished chunk j-1, and every
             // warp chunk j-lead (no warp runs further ahead: ring safety, tri_plan.hpp)
             if (lane < NW) {
@@ -398,9 +394,9 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 const double* dg = reinterpret_cast<const double*>(blob + kDiag);
                 const double* val = dg + mp;
                 const int* dep = reinterpret_cast<const int*>(val + W * mp);
-                const int* xidx = dep + (W + 1) * mp;
+                const int* xidx = dep + W * mp;
                 const int* exl = xidx + mp;
-                const double* bst = reinterpret_cast<const double*>(blob) - mp;
+                const double* bst = reinterpret_cast<const double*>(blob) - ((h0.x + 4) & ~3) + ((flags >> 5) & 1);
                 const double* hb = reinterpret_cast<const double*>(blob + reinterpret_cast<const int*>(blob)[7]) - (R + 1);
                 // one row per lane (the layout splits chunks so a warp never has more than 32)
                 const bool act = t0 + lane < t1;
@@ -474,6 +470,20 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
             __threadfence();
         }
     }
+}
+
+__global__ void k_permute_in(const double* __restrict__ b, const int* __restrict__ bidx, double* __restrict__ bp,
+                             int n) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) bp[r] = __ldg(b + bidx[r]);
+}
+
+void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = std::min((n + 255) / 256, sms * 8);
+    k_permute_in<<<blocks, 256, 0, st>>>(b, bidx, bp, n);
 }
 
 #define HEC_WAVE_INST(WD)                                    \

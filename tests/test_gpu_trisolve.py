@@ -159,3 +159,41 @@ def test_empty_and_single(H):
     empty = H.CsrMatrix.from_arrays(0, 0, np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0))
     p = H.prepare_lower(empty)
     assert H.solve(p, np.zeros(0)).shape == (0,)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_permute_in_then_ordered_solve(H, orc, strategy):
+    # hec_tri_permute_in + hec_tri_solve_ordered == hec_tri_solve, bitwise
+    torch = pytest.importorskip("torch")
+    for gen, dims in (("gen_poisson7", (20, 17, 9)), ("gen_poisson27", (9, 8, 7))):
+        a = getattr(H, gen)(*dims)
+        f = H.ilu0(a)
+        rng = np.random.default_rng(17)
+        for fac, upper in ((f.l, False), (f.u, True)):
+            p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+            t = H.DeviceTri.create(p, strategy=strategy)
+            b = rng.uniform(-1, 1, a.n_rows)
+            want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+            bd = torch.tensor(b, device="cuda")
+            bp = torch.full((a.n_rows + 2,), float("nan"), dtype=torch.float64, device="cuda")
+            x = torch.empty_like(bd)
+            t.permute_in(bd, bp)
+            t.solve_ordered(bp, x)
+            torch.cuda.synchronize()
+            assert bits_equal(x.cpu().numpy(), want)
+
+
+def test_wave_width_classes_and_splits(H, orc):
+    # every supported sliced-ELL width (1-8, 10, 13, 16) plus CSR tails, and
+    # chunks split at 32 rows per warp: ILU(k) / ILUT factors of a 27-point matrix
+    a = H.gen_poisson27(12, 11, 10)
+    rng = np.random.default_rng(5)
+    for fac in (H.ilu_k(a, 1), H.ilut(a, 20, 1e-4), H.ilut(a, 3, 1e-2)):
+        for t, upper in ((fac.l, False), (fac.u, True)):
+            for w in (1, 2, 3, 4, 5, 7, 8, 11, 16, 40):
+                p = (H.prepare_upper if upper else H.prepare_lower)(t, H.WidthPolicy.fixed(w))
+                b = rng.uniform(-1, 1, a.n_rows)
+                want = orc.solve(orc.prepare(to_oracle(t), upper=upper), b)
+                got, info = device_solve(H, p, b, 2, ctas=int(rng.integers(1, 40)))
+                assert info["strategy"] == 2
+                assert bits_equal(got, want), (w, upper)
