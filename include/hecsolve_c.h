@@ -142,6 +142,23 @@ int hec_precond_create(int n, int n_ext, const int* gather, const char* owned,
                        const double* u_ell_vals, const int* u_csr_row_offsets,
                        const int* u_csr_cols, const double* u_csr_vals,
                        const hec_tri_options* options, hec_precond_t* out);
+/*
+ * Local form for one RAS subdomain of a distributed vector (the multi-GPU
+ * layer): the input vector has n_in entries and factor row k reads
+ * r[gather[k]]; the output has n_out entries and factor row k writes
+ * x[out_index[k]] unless out_index[k] < 0 (rows the subdomain does not own).
+ * Replaces one block of hec::apply (proj/src/precond.cpp:125-143).
+ */
+int hec_precond_create_local(int n_in, int n_out, int n_ext, const int* gather, const int* out_index,
+                             /* L */ int l_nlev, const int* l_level_starts, const int* l_inv_perm,
+                             int l_ell_width, const int* l_ell_cols, const double* l_ell_vals,
+                             const int* l_csr_row_offsets, const int* l_csr_cols,
+                             const double* l_csr_vals,
+                             /* U (reversal applied) */ int u_nlev, const int* u_level_starts,
+                             const int* u_inv_perm, int u_ell_width, const int* u_ell_cols,
+                             const double* u_ell_vals, const int* u_csr_row_offsets,
+                             const int* u_csr_cols, const double* u_csr_vals,
+                             const hec_tri_options* options, hec_precond_t* out);
 int hec_precond_apply(hec_precond_t m, const double* r_dev, double* x_dev, void* stream);
 int hec_precond_apply_host(hec_precond_t m, const double* r, double* x);
 int hec_precond_query(hec_precond_t m, hec_tri_info* l_info, hec_tri_info* u_info);
@@ -178,6 +195,23 @@ int hec_gmres_solve(hec_spmv_t a, hec_precond_t m, const double* b, const hec_gm
                     double* x, hec_gmres_report* report, double* inner_residuals,
                     int inner_capacity);
 
+/*
+ * Fused Krylov vector kernels of the device GMRES (proj/src/gmres.cpp:63-80,
+ * 120-124), exposed for drivers that reduce across GPUs themselves (RAS).
+ * All scalars are device pointers; dots use a fixed-shape reduction.
+ */
+typedef struct hec_krylov* hec_krylov_t;
+int hec_krylov_create(int n, hec_krylov_t* out);
+/* w -= (*h_prev) * v_prev (skipped if v_prev == NULL); *out = dot(w, v_next) */
+int hec_krylov_mgs(hec_krylov_t k, double* w, const double* v_prev, const double* h_prev,
+                   const double* v_next, double* out, void* stream);
+int hec_krylov_scale(hec_krylov_t k, double* y, const double* x, const double* s, void* stream); /* y = x / *s */
+int hec_krylov_combine(hec_krylov_t k, int j, double* xc, const double* V, long long ldv,
+                       const double* y, void* stream);                                  /* xc = sum_i<j y_i V_i */
+int hec_krylov_add(hec_krylov_t k, double* x, const double* d, void* stream);           /* x += d */
+int hec_krylov_sqrt(hec_krylov_t k, const double* in, double* out, void* stream);       /* *out = sqrt(*in) */
+int hec_krylov_destroy(hec_krylov_t k);
+
 /* ===================== Section 2: host setup ============================= */
 
 typedef struct hec_csr* hec_csr_t;   /* owns a hec::CsrMatrix */
@@ -197,6 +231,18 @@ int hec_gen_poisson27(int nx, int ny, int nz, hec_csr_t* out);
 int hec_gen_reservoir7(int nx, int ny, int nz, double sigma, double kz_ratio, uint64_t seed,
                        hec_csr_t* out);
 int hec_permute_symmetric(hec_csr_t a, const int* perm, hec_csr_t* out);
+/* principal submatrix on the ascending row set rows[count] (reference
+ * precond.cpp:13-34, extract_block) */
+int hec_csr_submatrix(hec_csr_t a, const int* rows, int count, hec_csr_t* out);
+
+/* hec::partition_graph + hec::extend_overlap (reference partition.cpp:28-107):
+ * part_of[n]; extended part p = ext_rows[ext_offsets[p] .. ext_offsets[p+1]),
+ * ascending. Borrowed views valid until hec_partition_destroy. */
+typedef struct hec_partition* hec_partition_t;
+int hec_partition_create(hec_csr_t a, int parts, int overlap, hec_partition_t* out);
+int hec_partition_view(hec_partition_t p, int* n, int* parts, const int** part_of,
+                       const int** ext_offsets, const int** ext_rows);
+int hec_partition_destroy(hec_partition_t p);
 int hec_random_ordering(int n, uint64_t seed, int* perm);
 int hec_rcm_ordering(hec_csr_t a, int* perm);
 

@@ -83,7 +83,18 @@ _sig("hec_precond_create", c_int, c_int, c_int, P_int, P_char,
      c_int, P_int, P_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl,
      c_int, P_int, P_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl,
      C.POINTER(TriOptions), C.POINTER(c_void_p))
+_sig("hec_precond_create_local", c_int, c_int, c_int, c_int, P_int, P_int,
+     c_int, P_int, P_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl,
+     c_int, P_int, P_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl,
+     C.POINTER(TriOptions), C.POINTER(c_void_p))
 _sig("hec_precond_apply", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_krylov_create", c_int, c_int, C.POINTER(c_void_p))
+_sig("hec_krylov_mgs", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_krylov_scale", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_krylov_combine", c_int, c_void_p, c_int, c_void_p, c_void_p, c_ll, c_void_p, c_void_p)
+_sig("hec_krylov_add", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_krylov_sqrt", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_krylov_destroy", c_int, c_void_p)
 _sig("hec_precond_apply_host", c_int, c_void_p, P_dbl, P_dbl)
 _sig("hec_precond_query", c_int, c_void_p, C.POINTER(TriInfo), C.POINTER(TriInfo))
 _sig("hec_precond_destroy", c_int, c_void_p)
@@ -103,6 +114,10 @@ _sig("hec_gen_poisson7", c_int, c_int, c_int, c_int, C.POINTER(c_void_p))
 _sig("hec_gen_poisson27", c_int, c_int, c_int, c_int, C.POINTER(c_void_p))
 _sig("hec_gen_reservoir7", c_int, c_int, c_int, c_int, c_dbl, c_dbl, C.c_uint64, C.POINTER(c_void_p))
 _sig("hec_permute_symmetric", c_int, c_void_p, P_int, C.POINTER(c_void_p))
+_sig("hec_csr_submatrix", c_int, c_void_p, P_int, c_int, C.POINTER(c_void_p))
+_sig("hec_partition_create", c_int, c_void_p, c_int, c_int, C.POINTER(c_void_p))
+_sig("hec_partition_view", c_int, c_void_p, P_int, P_int, PP_int, PP_int, PP_int)
+_sig("hec_partition_destroy", c_int, c_void_p)
 _sig("hec_random_ordering", c_int, c_int, C.c_uint64, P_int)
 _sig("hec_rcm_ordering", c_int, c_void_p, P_int)
 _sig("hec_ilu0", c_int, c_void_p, C.POINTER(c_void_p), C.POINTER(c_void_p))
@@ -129,7 +144,10 @@ EXPORTED = [
     "hec_last_error", "hec_last_error_row", "hec_last_error_block", "hec_version", "hec_device_available",
     "hec_tri_create", "hec_tri_solve", "hec_tri_permute_in", "hec_tri_solve_ordered", "hec_tri_solve_host", "hec_tri_query", "hec_tri_destroy",
     "hec_tri_solve_traced",
-    "hec_precond_create", "hec_precond_apply", "hec_precond_apply_host", "hec_precond_query",
+    "hec_precond_create", "hec_precond_create_local", "hec_precond_apply", "hec_precond_apply_host",
+    "hec_precond_query", "hec_krylov_create", "hec_krylov_mgs", "hec_krylov_scale", "hec_krylov_combine",
+    "hec_krylov_add", "hec_krylov_sqrt", "hec_krylov_destroy", "hec_csr_submatrix", "hec_partition_create",
+    "hec_partition_view", "hec_partition_destroy",
     "hec_precond_destroy", "hec_spmv_create", "hec_spmv_run", "hec_spmv_run_host", "hec_spmv_destroy",
     "hec_gmres_solve", "hec_csr_create", "hec_csr_from_triples", "hec_csr_view", "hec_csr_destroy",
     "hec_csr_spmv_host", "hec_gen_poisson7", "hec_gen_poisson27", "hec_gen_reservoir7",

@@ -130,6 +130,64 @@ def permute_symmetric(a: CsrMatrix, perm) -> CsrMatrix:
     return _gen(lib.hec_permute_symmetric, a.handle, _p_int(p))
 
 
+def csr_submatrix(a: CsrMatrix, rows) -> CsrMatrix:
+    """Principal submatrix on ascending `rows` (reference precond.cpp:13-34)."""
+    r = np.ascontiguousarray(rows, dtype=_i32)
+    h = C.c_void_p()
+    check(lib.hec_csr_submatrix(a.handle, _p_int(r), r.shape[0], C.byref(h)))
+    return CsrMatrix(h)
+
+
+def partition(a: CsrMatrix, parts: int, overlap: int):
+    """hec::partition_graph + hec::extend_overlap (reference partition.cpp:28-107).
+    Returns (part_of[n], [ascending extended rows of part p for p < parts])."""
+    h = C.c_void_p()
+    check(lib.hec_partition_create(a.handle, parts, overlap, C.byref(h)))
+    try:
+        n, np_ = C.c_int(), C.c_int()
+        po, eo, er = L.P_int(), L.P_int(), L.P_int()
+        check(lib.hec_partition_view(h, C.byref(n), C.byref(np_), C.byref(po), C.byref(eo), C.byref(er)))
+        part_of = _view(po, n.value, _i32).copy()
+        offs = _view(eo, np_.value + 1, _i32).copy()
+        rows = _view(er, int(offs[-1]), _i32).copy()
+        return part_of, [rows[offs[p]:offs[p + 1]] for p in range(np_.value)]
+    finally:
+        lib.hec_partition_destroy(h)
+
+
+class Krylov:
+    """The fused Krylov vector kernels (hec_krylov_*), device pointers / tensors."""
+
+    def __init__(self, n: int):
+        self.n = n
+        self._h = C.c_void_p()
+        check(lib.hec_krylov_create(n, C.byref(self._h)))
+
+    def mgs(self, w, v_prev, h_prev, v_next, out, stream=None):
+        check(lib.hec_krylov_mgs(self._h, C.c_void_p(_ptr(w)), C.c_void_p(_ptr(v_prev) if v_prev is not None else None),
+                                 C.c_void_p(_ptr(h_prev) if h_prev is not None else None),
+                                 C.c_void_p(_ptr(v_next)), C.c_void_p(_ptr(out)), C.c_void_p(_stream(stream))))
+
+    def scale(self, y, x, s, stream=None):
+        check(lib.hec_krylov_scale(self._h, C.c_void_p(_ptr(y)), C.c_void_p(_ptr(x)), C.c_void_p(_ptr(s)),
+                                   C.c_void_p(_stream(stream))))
+
+    def combine(self, j, xc, V, ldv, y, stream=None):
+        check(lib.hec_krylov_combine(self._h, j, C.c_void_p(_ptr(xc)), C.c_void_p(_ptr(V)), ldv,
+                                     C.c_void_p(_ptr(y)), C.c_void_p(_stream(stream))))
+
+    def add(self, x, d, stream=None):
+        check(lib.hec_krylov_add(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(d)), C.c_void_p(_stream(stream))))
+
+    def sqrt(self, a, out, stream=None):
+        check(lib.hec_krylov_sqrt(self._h, C.c_void_p(_ptr(a)), C.c_void_p(_ptr(out)), C.c_void_p(_stream(stream))))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.hec_krylov_destroy(self._h)
+            self._h = None
+
+
 def random_ordering(n, seed=1606) -> np.ndarray:
     p = np.empty(n, dtype=_i32)
     check(lib.hec_random_ordering(n, seed, _p_int(p)))
@@ -390,6 +448,27 @@ class DevicePrecond:
                      _p_dbl(e.csr_values)]
         check(lib.hec_precond_create(n, pl.n, _p_int(g), o.ctypes.data_as(L.P_char) if o is not None else None,
                                      *args, C.byref(opt), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def create_local(cls, n_in, n_out, pl: PreparedTriangular, pu: PreparedTriangular, gather, out_index,
+                     strategy=L.STRATEGY_AUTO, ctas=0, threads=0):
+        """One RAS subdomain of a distributed vector: factor row k reads r[gather[k]]
+        and writes x[out_index[k]] (skipped when negative); see hec_precond_create_local."""
+        opt = L.TriOptions(strategy, ctas, threads)
+        g = np.ascontiguousarray(gather, dtype=_i32)
+        o = np.ascontiguousarray(out_index, dtype=_i32)
+        if g.shape[0] != pl.n or o.shape[0] != pl.n:
+            raise ValueError("create_local: map size must equal the factor size")
+        h = C.c_void_p()
+        args = []
+        for p in (pl, pu):
+            s, e = p.schedule, p.hec
+            args += [s.nlev, _p_int(s.level_starts), _p_int(s.inv_perm), e.ell.width, _p_int(e.ell.col_indices),
+                     _p_dbl(e.ell.values), _p_int(e.csr_row_offsets), _p_int(e.csr_col_indices),
+                     _p_dbl(e.csr_values)]
+        check(lib.hec_precond_create_local(n_in, n_out, pl.n, _p_int(g), _p_int(o), *args, C.byref(opt),
+                                           C.byref(h)))
         return cls(h)
 
     def apply(self, r_dev, x_dev, stream=None) -> None:

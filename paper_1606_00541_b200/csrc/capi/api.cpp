@@ -44,6 +44,13 @@ struct hec_bp {
     hec::BlockPreconditioner m;
     hec_prep l, u;
 };
+struct hec_krylov {
+    std::unique_ptr<hec::dev::KrylovOps> impl;
+};
+struct hec_partition {
+    int n = 0, parts = 0;
+    std::vector<int> part_of, ext_offsets, ext_rows;
+};
 
 namespace hec {
 
@@ -382,6 +389,73 @@ int hec_precond_create(int n, int n_ext, const int* gather, const char* owned, i
     });
 }
 
+int hec_precond_create_local(int n_in, int n_out, int n_ext, const int* gather, const int* out_index, int l_nlev,
+                             const int* l_level_starts, const int* l_inv_perm, int l_ell_width, const int* l_ell_cols,
+                             const double* l_ell_vals, const int* l_csr_row_offsets, const int* l_csr_cols,
+                             const double* l_csr_vals, int u_nlev, const int* u_level_starts, const int* u_inv_perm,
+                             int u_ell_width, const int* u_ell_cols, const double* u_ell_vals,
+                             const int* u_csr_row_offsets, const int* u_csr_cols, const double* u_csr_vals,
+                             const hec_tri_options* options, hec_precond_t* out) {
+    return guarded([&] {
+        need(out, "hec_precond_create_local");
+        auto h = std::make_unique<hec_precond>();
+        h->impl = std::make_unique<hec::dev::DevicePrecond>(
+            n_in, n_out, n_ext, gather, out_index,
+            raw_source(n_ext, 0, l_nlev, l_level_starts, l_inv_perm, l_ell_width, l_ell_cols, l_ell_vals,
+                       l_csr_row_offsets, l_csr_cols, l_csr_vals),
+            raw_source(n_ext, 1, u_nlev, u_level_starts, u_inv_perm, u_ell_width, u_ell_cols, u_ell_vals,
+                       u_csr_row_offsets, u_csr_cols, u_csr_vals),
+            hec::tri_options(options));
+        *out = h.release();
+    });
+}
+
+int hec_krylov_create(int n, hec_krylov_t* out) {
+    return guarded([&] {
+        need(out, "hec_krylov_create");
+        hec::dev::require_device();
+        auto h = std::make_unique<hec_krylov>();
+        h->impl = std::make_unique<hec::dev::KrylovOps>(n);
+        *out = h.release();
+    });
+}
+int hec_krylov_mgs(hec_krylov_t k, double* w, const double* v_prev, const double* h_prev, const double* v_next,
+                   double* out, void* stream) {
+    return guarded([&] {
+        need(k, "hec_krylov_mgs");
+        if (v_prev && !h_prev) throw std::invalid_argument("hec_krylov_mgs: v_prev needs h_prev");
+        k->impl->mgs(w, v_prev, h_prev, v_next, out, static_cast<cudaStream_t>(stream));
+    });
+}
+int hec_krylov_scale(hec_krylov_t k, double* y, const double* x, const double* s, void* stream) {
+    return guarded([&] {
+        need(k, "hec_krylov_scale");
+        k->impl->scale(y, x, s, static_cast<cudaStream_t>(stream));
+    });
+}
+int hec_krylov_combine(hec_krylov_t k, int j, double* xc, const double* V, long long ldv, const double* y,
+                       void* stream) {
+    return guarded([&] {
+        need(k, "hec_krylov_combine");
+        k->impl->combine(j, xc, V, ldv, y, static_cast<cudaStream_t>(stream));
+    });
+}
+int hec_krylov_add(hec_krylov_t k, double* x, const double* d, void* stream) {
+    return guarded([&] {
+        need(k, "hec_krylov_add");
+        k->impl->add(x, d, static_cast<cudaStream_t>(stream));
+    });
+}
+int hec_krylov_sqrt(hec_krylov_t k, const double* in, double* out, void* stream) {
+    return guarded([&] {
+        need(k, "hec_krylov_sqrt");
+        k->impl->sqrt(in, out, static_cast<cudaStream_t>(stream));
+    });
+}
+int hec_krylov_destroy(hec_krylov_t k) {
+    return guarded([&] { delete k; });
+}
+
 int hec_precond_apply(hec_precond_t m, const double* r_dev, double* x_dev, void* stream) {
     return guarded([&] {
         need(m, "hec_precond_apply");
@@ -531,6 +605,57 @@ int hec_gen_reservoir7(int nx, int ny, int nz, double sigma, double kz_ratio, ui
 int hec_permute_symmetric(hec_csr_t a, const int* perm, hec_csr_t* out) {
     need(a, "hec_permute_symmetric");
     HEC_WRAP_GEN(hec::permute_symmetric(a->m, std::vector<int>(perm, perm + a->m.n_rows)));
+}
+
+int hec_csr_submatrix(hec_csr_t a, const int* rows, int count, hec_csr_t* out) {
+    return guarded([&] {
+        need(a, "hec_csr_submatrix");
+        need(out, "hec_csr_submatrix");
+        if (count < 0 || (count > 0 && !rows)) throw std::invalid_argument("hec_csr_submatrix: bad row set");
+        std::vector<int> r(rows, rows + count);
+        for (int k = 0; k < count; ++k) {
+            if (r[k] < 0 || r[k] >= a->m.n_rows) throw std::out_of_range("hec_csr_submatrix: row out of range");
+            if (k && r[k] <= r[k - 1]) throw std::invalid_argument("hec_csr_submatrix: rows must ascend");
+        }
+        auto h = std::make_unique<hec_csr>();
+        h->m = hec::extract_block(a->m, r);
+        *out = h.release();
+    });
+}
+
+int hec_partition_create(hec_csr_t a, int parts, int overlap, hec_partition_t* out) {
+    return guarded([&] {
+        need(a, "hec_partition_create");
+        need(out, "hec_partition_create");
+        const hec::Partition p = hec::partition_graph(a->m, parts);
+        const auto ext = hec::extend_overlap(a->m, p, overlap);
+        auto h = std::make_unique<hec_partition>();
+        h->n = p.n;
+        h->parts = p.n_parts;
+        h->part_of = p.part_of;
+        h->ext_offsets.assign(1, 0);
+        for (const auto& e : ext) {
+            h->ext_rows.insert(h->ext_rows.end(), e.begin(), e.end());
+            h->ext_offsets.push_back(static_cast<int>(h->ext_rows.size()));
+        }
+        *out = h.release();
+    });
+}
+
+int hec_partition_view(hec_partition_t p, int* n, int* parts, const int** part_of, const int** ext_offsets,
+                       const int** ext_rows) {
+    return guarded([&] {
+        need(p, "hec_partition_view");
+        if (n) *n = p->n;
+        if (parts) *parts = p->parts;
+        if (part_of) *part_of = p->part_of.data();
+        if (ext_offsets) *ext_offsets = p->ext_offsets.data();
+        if (ext_rows) *ext_rows = p->ext_rows.data();
+    });
+}
+
+int hec_partition_destroy(hec_partition_t p) {
+    return guarded([&] { delete p; });
 }
 
 int hec_random_ordering(int n, uint64_t seed, int* perm) {

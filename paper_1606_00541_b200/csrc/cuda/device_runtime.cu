@@ -249,9 +249,31 @@ void DeviceTri::solve_host(const double* b, double* x) {
 }
 
 // -------------------------------------------------------- DevicePrecond ----
+DevicePrecond::DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, const int* out_index,
+                             plan::TriSource l, plan::TriSource u, const TriOptions& opt)
+    : n_(n_in), n_out_(n_out), n_ext_(n_ext) {
+    require_device();
+    identity_ = false;
+    if (n_in < 0 || n_out < 0 || n_ext < 0) throw std::invalid_argument("hec_precond_create_local: negative size");
+    if (l.n != n_ext || u.n != n_ext) throw std::invalid_argument("hec_precond_create_local: factor size mismatch");
+    if (n_ext > 0 && (!gather || !out_index)) throw std::invalid_argument("hec_precond_create_local: missing map");
+    std::vector<int> hits(static_cast<std::size_t>(n_out), 0);
+    for (int k = 0; k < n_ext; ++k) {
+        if (gather[k] < 0 || gather[k] >= n_in)
+            throw std::invalid_argument("hec_precond_create_local: gather out of range");
+        if (out_index[k] >= n_out) throw std::invalid_argument("hec_precond_create_local: output index out of range");
+        if (out_index[k] >= 0 && ++hits[out_index[k]] > 1)
+            throw std::invalid_argument("hec_precond_create_local: output row written twice");
+    }
+    l.b_map = gather;
+    u.out_map = out_index;
+    l_ = std::make_unique<DeviceTri>(l, opt);
+    u_ = std::make_unique<DeviceTri>(u, opt);
+}
+
 DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
                              plan::TriSource u, const TriOptions& opt)
-    : n_(n), n_ext_(n_ext) {
+    : n_(n), n_out_(n), n_ext_(n_ext) {
     require_device();
     identity_ = gather == nullptr;
     if (identity_ && n_ext != n) throw std::invalid_argument("hec_precond_create: identity map needs n_ext == n");
@@ -291,7 +313,7 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
 }
 
 void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
-    if (n_ == 0) return;
+    if (n_ext_ == 0) return;
     Workspace& w = workspace(st);
     l_->solve(r, w.y.p, nullptr, st);
     if (identity_)
@@ -301,17 +323,14 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
 }
 
 void DevicePrecond::apply_host(const double* r, double* x) {
-    if (n_ == 0) return;
+    if (n_ == 0 && n_out_ == 0) return;
     std::lock_guard<std::mutex> g(h_mu_);
     if (!h_stream_) HEC_CUDA(cudaStreamCreateWithFlags(&h_stream_, cudaStreamNonBlocking));
-    if (h_r_.count < static_cast<std::size_t>(n_)) {
-        h_r_.alloc(n_);
-        h_x_.alloc(n_);
-    }
-    const std::size_t bytes = sizeof(double) * n_;
-    HEC_CUDA(cudaMemcpyAsync(h_r_.p, r, bytes, cudaMemcpyHostToDevice, h_stream_));
+    if (h_r_.count < static_cast<std::size_t>(std::max(n_, 1))) h_r_.alloc(std::max(n_, 1));
+    if (h_x_.count < static_cast<std::size_t>(std::max(n_out_, 1))) h_x_.alloc(std::max(n_out_, 1));
+    HEC_CUDA(cudaMemcpyAsync(h_r_.p, r, sizeof(double) * n_, cudaMemcpyHostToDevice, h_stream_));
     apply(h_r_.p, h_x_.p, h_stream_);
-    HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, bytes, cudaMemcpyDeviceToHost, h_stream_));
+    HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, sizeof(double) * n_out_, cudaMemcpyDeviceToHost, h_stream_));
     HEC_CUDA(cudaStreamSynchronize(h_stream_));
 }
 

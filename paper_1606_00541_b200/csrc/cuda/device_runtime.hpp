@@ -135,17 +135,23 @@ public:
     // l/u sources carry no maps; they are attached here from gather/owned.
     DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
                   plan::TriSource u, const TriOptions& opt);
+    // Local form (one RAS subdomain of a distributed vector): the input has n_in
+    // entries and row k of the factors reads r[gather[k]]; the output has n_out
+    // entries and row k writes x[out_index[k]] unless out_index[k] < 0.
+    DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, const int* out_index, plan::TriSource l,
+                  plan::TriSource u, const TriOptions& opt);
     void apply(const double* r, double* x, cudaStream_t st);
     void apply_host(const double* r, double* x);
     const DeviceTri& lower() const { return *l_; }
     const DeviceTri& upper() const { return *u_; }
     int n() const { return n_; }
+    int n_out() const { return n_out_; }
 
 private:
     struct Workspace {
         DevBuf<double> y, z;
     };
-    int n_ = 0, n_ext_ = 0;
+    int n_ = 0, n_out_ = 0, n_ext_ = 0;
     bool identity_ = true;
     std::unique_ptr<DeviceTri> l_, u_;
     std::mutex mu_;

@@ -98,7 +98,51 @@ __global__ void k_add(int n, double* x, const double* d) {
         x[i] = __dadd_rn(x[i], d[i]);
 }
 
+__global__ void k_sqrt(const double* in, double* out) { *out = __dsqrt_rn(*in); }
+
 }  // namespace
+
+KrylovOps::KrylovOps(int n) : n_(n) {
+    if (n < 0) throw std::invalid_argument("hec_krylov_create: negative size");
+    int dev = 0, sms = 0;
+    HEC_CUDA(cudaGetDevice(&dev));
+    HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid_ = std::max(1, std::min(2 * sms, (n + kThreads - 1) / kThreads));
+    HEC_CUDA(cudaMalloc(reinterpret_cast<void**>(&partials_), sizeof(double) * grid_));
+    HEC_CUDA(cudaMalloc(reinterpret_cast<void**>(&counter_), sizeof(unsigned)));
+    HEC_CUDA(cudaMemset(counter_, 0, sizeof(unsigned)));
+}
+
+KrylovOps::~KrylovOps() {
+    cudaFree(partials_);
+    cudaFree(counter_);
+}
+
+void KrylovOps::mgs(double* w, const double* v_prev, const double* h_prev, const double* v_next, double* out,
+                    cudaStream_t st) {
+    k_mgs_step<<<grid_, kThreads, 0, st>>>(n_, w, v_prev, h_prev, v_next, partials_, counter_, out, nullptr);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void KrylovOps::scale(double* y, const double* x, const double* s, cudaStream_t st) {
+    k_div<<<grid_, kThreads, 0, st>>>(n_, y, x, s);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void KrylovOps::combine(int j, double* xc, const double* V, long long ldv, const double* y, cudaStream_t st) {
+    k_combine<<<grid_, kThreads, 0, st>>>(n_, j, xc, V, static_cast<size_t>(ldv), y);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void KrylovOps::add(double* x, const double* d, cudaStream_t st) {
+    k_add<<<grid_, kThreads, 0, st>>>(n_, x, d);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void KrylovOps::sqrt(const double* in, double* out, cudaStream_t st) {
+    k_sqrt<<<1, 1, 0, st>>>(in, out);
+    HEC_CUDA(cudaGetLastError());
+}
 
 GmresOutcome gmres_device(const DeviceSpmv& A, DevicePrecond* M, const double* b_host, const GmresParams& cfg,
                           double* x_host) {
