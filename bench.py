@@ -20,7 +20,9 @@ Metric: effective HBM GB/s = B_alg / time with B_alg = sum over L,U of
 
 Multi-GPU (torchrun): the single triangular solve does not shard (SURVEY.md
 8(e)), so N ranks run N independent replicas; value = N * B_alg / max-over-
-ranks step time ("scaling": "weak").
+ranks step time ("scaling": "weak"). The RAS half of the metric does shard:
+the "ras" object is RAS-ILU(0) GMRES(30) time-to-solution on 7-pt 256^3 with
+one subdomain per GPU (NCCL halo all-to-all + dot all-reduces), max over ranks.
 """
 from __future__ import annotations
 
@@ -392,6 +394,38 @@ def secondary_device(H, torch, device, steps):
             "target_ms_for_50pct": round(alg / (0.5 * peak * 1e9) * 1e3, 4)}
 
 
+def ras_gmres(H, torch, rank, world, device, size, restart=30):
+    """RAS-ILU(0) GMRES(restart) time-to-solution, one subdomain per GPU
+    (BASELINE config 4; paper_1606_00541_b200/ras.py). Max over ranks."""
+    from paper_1606_00541_b200 import ras
+    t0 = time.time()
+    a = H.gen_poisson7(size, size, size)
+    b = H.spmv_csr(a, np.ones(a.n_rows), workers=os.cpu_count())
+    solver = ras.RasGmres(a, overlap=1, restart=restart, device=device)
+    setup = time.time() - t0
+    solver.solve(b)  # warm-up: device layouts, workspaces, NCCL channels
+    torch.cuda.synchronize(device)
+    if world > 1:
+        torch.distributed.barrier()
+    t1 = time.perf_counter()
+    x, rep = solver.solve(b)
+    torch.cuda.synchronize(device)
+    sec = time.perf_counter() - t1
+    err = float((x - 1.0).abs().max().item())
+    if world > 1:
+        t = torch.tensor([sec, err], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        sec, err = float(t[0].item()), float(t[1].item())
+    log(f"[bench] RAS {size}^3 x{world}: {rep.iterations} iterations in {sec*1e3:.1f} ms (setup {setup:.1f}s)")
+    return {"workload": f"RAS-ILU(0) GMRES({restart}), 7-pt Poisson {size}^3, overlap 1, {world} block(s) = GPU(s), "
+                        f"b = A*1, rel_tol 1e-6",
+            "seconds": round(sec, 5), "iterations": rep.iterations, "converged": rep.converged,
+            "final_relative_residual": rep.final_relative_residual, "ms_per_iteration": round(1e3 * sec / max(rep.iterations, 1), 4),
+            "max_abs_error_vs_ones": err, "allreduces": rep.allreduces, "halo_exchanges": rep.exchanges,
+            "rows_per_gpu": solver.plan.n_own, "halo_rows": int(len(solver.plan.halo)),
+            "collectives": "NCCL all_reduce (dots) + all_to_all_single (halo)" if world > 1 else "none"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -401,6 +435,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
+    ap.add_argument("--ras-size", type=int, default=256, help="grid edge of the RAS GMRES run (0 = skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -437,6 +472,10 @@ def main():
         if not args.no_secondary and args.config != "c4":
             del a, f, pl, pu
             result["secondary"] = secondary_device(H, torch, device, max(5, min(args.steps, 20)))
+        import gc
+        gc.collect()
+    if args.ras_size > 0:
+        result["ras"] = ras_gmres(H, torch, rank, world, device, args.ras_size)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
