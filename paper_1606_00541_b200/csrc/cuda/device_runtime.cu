@@ -65,8 +65,9 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
     strategy_ = opt.strategy == 1 ? 1 : 2;
     if (strategy_ == 2 && n_ > 0) {
         plan::WaveConfig cfg;
-        cfg.ctas = opt.ctas > 0 ? opt.ctas : sm_count();
+        cfg.ctas = opt.ctas > 0 ? std::min(opt.ctas, sm_count()) : sm_count();  // one resident CTA per SM
         cfg.warps = kWaveSolverWarps;
+        if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
         cfg.warp_rows = 32;  // one row per lane
         const int budget = smem_optin() - 1024;  // static shared + slack
         plan::WaveLayout P;
@@ -85,10 +86,11 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_inflight_ = P.inflight;
             p_lead_ = P.lead;
             if (std::getenv("HEC_DEBUG"))
-                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d max_region=%d buf=%d exports=%lld "
-                             "deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n, P.chunks, P.ctas, P.warps,
-                             P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps, P.halo_deps,
-                             P.halo_values);
+                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d W=%d %s grid=%dx%d max_region=%d "
+                             "buf=%d exports=%lld deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n,
+                             P.chunks, P.ctas, P.warps, P.max_width, P.pencils ? "pencils" : "slabs", P.grid_nx,
+                             P.grid_ny, P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps,
+                             P.halo_deps, P.halo_values);
             p_smem_ = p_buf_off_ + p_buf_bytes_;
             p_ctas_ = P.ctas;
             p_kernel_ = wave_kernel(P.max_width, false);
@@ -229,8 +231,9 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
     a.buf_bytes = p_buf_bytes_;
     a.trace = trace;
     void* args[] = {&a};
-    HEC_CUDA(cudaLaunchKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_),
-                              dim3(kWaveRoleThreads + 32 * p_warps_), args, p_smem_, st));
+    // cooperative: every CTA resident at once (CTAs wait on each other's rows)
+    HEC_CUDA(cudaLaunchCooperativeKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_),
+                                         dim3(kWaveRoleThreads + 32 * p_warps_), args, p_smem_, st));
 }
 
 void DeviceTri::solve_host(const double* b, double* x) {

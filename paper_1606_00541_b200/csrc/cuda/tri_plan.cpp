@@ -8,6 +8,7 @@
 #include "tri_plan.hpp"
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -39,6 +40,82 @@ inline int entry_count(const TriSource& s, int r) {
     for (int k = 0; k < s.ell_width; ++k)
         if (s.ell_cols[static_cast<std::size_t>(k) * s.n + r] != r) ++cnt;
     return cnt + (s.csr_rp[r + 1] - s.csr_rp[r] - 1);
+}
+
+// ---- structured-grid recognition (pencil ownership) ----
+struct GridGeom {
+    bool ok = false;
+    int nx = 0, ny = 0, nz = 0;
+};
+
+// The factor of a 7- or 27-point stencil on an nx x ny x nz grid in natural
+// order has, in the lower frame, dependency offsets {1, nx, nx*ny} or
+// {1, nx-1..nx+1, nx*ny-nx-1 .. nx*ny+nx+1} on almost every row. Recognise
+// them on a sample of rows; anything else keeps the slab ownership.
+GridGeom detect_grid(const TriSource& s) {
+    GridGeom g;
+    const int n = s.n;
+    if (n < 4096) return g;
+    std::unordered_map<int, long long> freq;
+    const int step = std::max(1, n / 100000);
+    long long rows = 0;
+    for (int r = 0; r < n; r += step) {
+        const int i = s.inv_perm[r];
+        ++rows;
+        for_each_entry(s, r, [&](int col, double) { ++freq[i - s.inv_perm[col]]; });
+    }
+    std::vector<int> frequent;
+    for (const auto& [d, c] : freq)
+        if (d > 0 && c * 2 >= rows) frequent.push_back(d);
+    std::sort(frequent.begin(), frequent.end());
+    if (frequent.size() < 3 || frequent[0] != 1) return g;
+    auto has = [&](int d) { return std::binary_search(frequent.begin(), frequent.end(), d); };
+    const int d2 = frequent[1];
+    const int nx = (has(d2 + 1) && has(d2 + 2)) ? d2 + 1 : d2;  // 27-point: nx-1, nx, nx+1
+    std::vector<int> big;
+    for (int d : frequent)
+        if (d > nx + 1) big.push_back(d);
+    if (big.empty()) return g;
+    const long long plane = (static_cast<long long>(big.front()) + big.back()) / 2;
+    if (nx < 4 || plane % nx != 0 || n % plane != 0) return g;
+    g.nx = nx;
+    g.ny = static_cast<int>(plane / nx);
+    g.nz = static_cast<int>(n / plane);
+    g.ok = g.ny >= 4 && g.nz >= 2;
+    return g;
+}
+
+// CTA tiles of (4 sx) x (4 sy) columns in x-y, each split into 4 x 4 warp
+// sub-tiles of sx x sy <= 32 columns (so a level never gives a warp more than
+// 32 rows): the most CTAs that fit C, ties to square sub-tiles.
+bool pencil_owners(const GridGeom& g, int n, int C, int NW, std::vector<int>& owner, std::vector<int>& warp,
+                   int& used) {
+    if (NW != 16) return false;
+    int best = -1, bsx = 0, bsy = 0, bpx = 0, bpy = 0;
+    for (int sx = 1; sx <= 32; ++sx)
+        for (int sy = 1; sx * sy <= 32; ++sy) {
+            const int px = (g.nx + 4 * sx - 1) / (4 * sx), py = (g.ny + 4 * sy - 1) / (4 * sy);
+            if (px * py > C || px < 2 || py < 2) continue;
+            const int score = px * py * 64 - std::abs(sx - sy);
+            if (score > best) {
+                best = score;
+                bsx = sx;
+                bsy = sy;
+                bpx = px;
+                bpy = py;
+            }
+        }
+    if (best < 0) return false;
+    const int tw = 4 * bsx, th = 4 * bsy;
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+        const int x = i % g.nx, y = (i / g.nx) % g.ny;
+        const int px = x / tw, py = y / th;
+        owner[i] = py * bpx + px;
+        warp[i] = ((y - py * th) / bsy) * 4 + (x - px * tw) / bsx;
+    }
+    used = bpx * bpy;
+    return true;
 }
 
 }  // namespace
@@ -119,43 +196,79 @@ LevelLayout build_levels(const TriSource& s) {
 WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     WaveLayout P;
     const int n = s.n;
-    const int C = std::max(1, std::min(cfg.ctas, std::max(n, 1)));
+    const int C0 = std::max(1, std::min(cfg.ctas, std::max(n, 1)));
     const int NW = std::max(1, std::min(cfg.warps, 32));
     const int R = cfg.ring;
     P.n = n;
     P.nlev = s.nlev;
-    P.ctas = C;
     P.warps = NW;
     P.ring = R;
     P.inflight = cfg.inflight;
     P.lead = std::max(1, std::min(cfg.lead, cfg.inflight));
     P.has_out = s.out_map != nullptr;
-    const int per = n > 0 ? (n + C - 1) / C : 1;
-    const int per_w = (per + NW - 1) / NW;
-    auto owner_of_i = [&](int i) { return std::min(i / per, C - 1); };
-    auto warp_of_i = [&](int i) { return std::min((i - owner_of_i(i) * per) / per_w, NW - 1); };
+    // ---- ownership: row -> (CTA, warp) in the lower frame
+    std::vector<int> owner_i(n), warp_i(n);
+    int C_used = C0;
+    const GridGeom geo = cfg.pencils ? detect_grid(s) : GridGeom{};
+    // pencils only when they shorten the per-CTA level chain (the most levels
+    // any CTA must walk through): true for 7-point stencils (levels x+y+z),
+    // not for 27-point ones (x+2y+4z: a z-pencil spans 4 nz levels)
+    auto max_levels_per_cta = [&](const std::vector<int>& own, int ncta) {
+        std::vector<int> lev_of_i(n);
+        for (int k = 0; k < s.nlev; ++k)
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) lev_of_i[s.inv_perm[r]] = k;
+        std::vector<int> lo(ncta, INT32_MAX), hi(ncta, -1);
+        for (int i = 0; i < n; ++i) {
+            lo[own[i]] = std::min(lo[own[i]], lev_of_i[i]);
+            hi[own[i]] = std::max(hi[own[i]], lev_of_i[i]);
+        }
+        int m = 0;
+        for (int c = 0; c < ncta; ++c)
+            if (hi[c] >= 0) m = std::max(m, hi[c] - lo[c] + 1);
+        return m;
+    };
+    bool use_pencils = false;
+    if (geo.ok && pencil_owners(geo, n, C0, NW, owner_i, warp_i, C_used)) {
+        const int per = (n + C0 - 1) / C0;
+        std::vector<int> slab(n);
+        for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
+        use_pencils = max_levels_per_cta(owner_i, C_used) < max_levels_per_cta(slab, C0);
+    }
+    if (use_pencils) {
+        P.pencils = true;
+        P.grid_nx = geo.nx;
+        P.grid_ny = geo.ny;
+    } else {
+        // slabs: CTA c owns [c*per, (c+1)*per), warps contiguous sub-ranges
+        const int per = n > 0 ? (n + C0 - 1) / C0 : 1;
+        const int per_w = (per + NW - 1) / NW;
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            owner_i[i] = std::min(i / per, C0 - 1);
+            warp_i[i] = std::min((i - owner_i[i] * per) / per_w, NW - 1);
+        }
+        C_used = C0;
+    }
+    P.ctas = C_used;
+    const int C = C_used;
 
     std::vector<int> cnt(n), owner_r(n), warp_r(n), nforeign(n, 0);
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < n; ++r) {
         cnt[r] = entry_count(s, r);
-        owner_r[r] = owner_of_i(s.inv_perm[r]);
-        warp_r[r] = warp_of_i(s.inv_perm[r]);
+        owner_r[r] = owner_i[s.inv_perm[r]];
+        warp_r[r] = warp_i[s.inv_perm[r]];
     }
-    // foreign dependencies must come from lower CTAs (ticket order = forward progress)
-    bool bad = false;
-#pragma omp parallel for schedule(static) reduction(|| : bad)
+    // cross-CTA dependencies: any direction (the kernel is launched cooperatively,
+    // so every CTA is resident; the level order keeps the waits acyclic)
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < n; ++r) {
         int f = 0;
         for_each_entry(s, r, [&](int col, double) {
-            if (owner_r[col] != owner_r[r]) {
-                ++f;
-                if (owner_r[col] > owner_r[r]) bad = true;
-            }
+            if (owner_r[col] != owner_r[r]) ++f;
         });
         nforeign[r] = f;
     }
-    if (bad) throw std::invalid_argument("hec_tri_create: wave layout needs dependencies on lower CTAs only");
 
     // 0. one sliced-ELL width W for the whole layout (every chunk padded to W, so
     //    the kernel's row loop is straight-line code): the supported width that
@@ -184,33 +297,46 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     const int W = P.max_width;
 
-    // 1. chunk discovery: per level, the run of each CTA, split so that no warp
-    //    has more than warp_rows rows in a chunk and by bytes
-    struct Chunk { int level, r0, m, w, ntail; };
+    // 1. chunk discovery: per level, each CTA's rows (ordered by warp, then by
+    //    row, so every warp's rows are one segment), split so that no warp has
+    //    more than warp_rows rows in a chunk and by bytes
+    struct Chunk { int level, row0, m, w, ntail; };  // rows: cta_rows[c][row0 .. row0+m)
     std::vector<std::vector<Chunk>> per_cta(C);
+    std::vector<std::vector<int>> cta_rows(C);
     const int fl_est = 4 | (P.has_out ? 2 : 0);
-    for (int k = 0; k < s.nlev; ++k) {
-        int r = s.level_starts[k];
-        const int re = s.level_starts[k + 1];
-        while (r < re) {
-            const int c = owner_r[r];
-            Chunk ch{k, r, 0, W, 0};
-            int halo_ub = 0, cur_w = -1, cur_cnt = 0;
-            while (r < re && owner_r[r] == c) {
-                const int t2 = ch.ntail + std::max(0, cnt[r] - W);
-                const int h2 = halo_ub + nforeign[r];
-                const int fl = fl_est | (t2 > 0 ? 1 : 0);
-                const int wcnt = warp_r[r] == cur_w ? cur_cnt + 1 : 1;
-                const int bytes = wave_region_bytes(ch.m + 1, h2, wave_sections(ch.m + 1, W, NW, h2, t2, fl).end);
-                if (ch.m > 0 && (wcnt > cfg.warp_rows || bytes > cfg.max_bytes)) break;
-                cur_w = warp_r[r];
-                cur_cnt = wcnt;
-                ch.ntail = t2;
-                halo_ub = h2;
-                ++ch.m;
-                ++r;
+    {
+        std::vector<std::vector<int>> bucket(C);
+        for (int k = 0; k < s.nlev; ++k) {
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) bucket[owner_r[r]].push_back(r);
+            for (int c = 0; c < C; ++c) {
+                auto& B = bucket[c];
+                if (B.empty()) continue;
+                std::stable_sort(B.begin(), B.end(), [&](int x, int y) { return warp_r[x] < warp_r[y]; });
+                std::size_t u = 0;
+                while (u < B.size()) {
+                    Chunk ch{k, static_cast<int>(cta_rows[c].size()), 0, W, 0};
+                    int halo_ub = 0, cur_w = -1, cur_cnt = 0;
+                    while (u < B.size()) {
+                        const int r = B[u];
+                        const int t2 = ch.ntail + std::max(0, cnt[r] - W);
+                        const int h2 = halo_ub + nforeign[r];
+                        const int fl = fl_est | (t2 > 0 ? 1 : 0);
+                        const int wcnt = warp_r[r] == cur_w ? cur_cnt + 1 : 1;
+                        const int bytes =
+                            wave_region_bytes(ch.m + 1, h2, wave_sections(ch.m + 1, W, NW, h2, t2, fl).end);
+                        if (ch.m > 0 && (wcnt > cfg.warp_rows || bytes > cfg.max_bytes)) break;
+                        cur_w = warp_r[r];
+                        cur_cnt = wcnt;
+                        ch.ntail = t2;
+                        halo_ub = h2;
+                        cta_rows[c].push_back(r);
+                        ++ch.m;
+                        ++u;
+                    }
+                    per_cta[c].push_back(ch);
+                }
+                B.clear();
             }
-            per_cta[c].push_back(ch);
         }
     }
 
@@ -225,8 +351,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         qend[c].resize(L.size());
         for (std::size_t j = 0; j < L.size(); ++j) {
             for (int t = 0; t < L[j].m; ++t) {
-                seq_r[L[j].r0 + t] = q + t;
-                chunk_pos_r[L[j].r0 + t] = static_cast<int>(j);
+                seq_r[cta_rows[c][L[j].row0 + t]] = q + t;
+                chunk_pos_r[cta_rows[c][L[j].row0 + t]] = static_cast<int>(j);
             }
             q += L[j].m;
             qend[c][j] = q;
@@ -241,12 +367,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     P.chunks = P.cta_chunk0[C];
 
-    // input index of every reordered row (the permute-in pass before the solve)
-    P.bidx.resize(n);
+    // wave order: (CTA, chunk, row in chunk); bp[wave position] = b[bidx[..]]
+    std::vector<long long> cta_wbase(static_cast<std::size_t>(C) + 1, 0);
+    for (int c = 0; c < C; ++c) cta_wbase[c + 1] = cta_wbase[c] + static_cast<long long>(cta_rows[c].size());
+    P.bidx.assign(n, 0);
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < n; ++r) {
         const int o = sol_index(s, r);
-        P.bidx[r] = s.b_map ? s.b_map[o] : o;
+        P.bidx[cta_wbase[owner_r[r]] + seq_r[r]] = s.b_map ? s.b_map[o] : o;
     }
 
     // 3. exports: rows read by another CTA get a mailbox id
@@ -296,7 +424,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             std::vector<int> t0(NW, -1), t1(NW, -1);
             bool glob = false, any_exp = false;
             for (int t = 0; t < m; ++t) {
-                const int r = ch.r0 + t;
+                const int r = cta_rows[c][ch.row0 + t];
                 const int wr = warp_r[r];
                 if (t0[wr] < 0) t0[wr] = t;
                 else if (t1[wr] != t) seg_bad[c] = 1;  // warp rows must be contiguous in the chunk
@@ -346,8 +474,9 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             const int ntail = static_cast<int>(tdep.size());
             st_hval[c] += nhalo;
             (void)any_exp;  // the export list is always present (-1 = row not exported)
+            const long long wpos = cta_wbase[c] + q0;  // wave position of the chunk's first row
             const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0) |
-                              ((ch.r0 & 1) ? 32 : 0);
+                              ((wpos & 1) ? 32 : 0);
             const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
             const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
@@ -364,7 +493,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             auto put_i = [&](int off, int idx, int v) { std::memcpy(b + off + 4 * idx, &v, 4); };
             auto put_d = [&](int off, int idx, double v) { std::memcpy(b + off + 8 * idx, &v, 8); };
             for (int t = 0; t < m; ++t) {
-                const int r = ch.r0 + t;
+                const int r = cta_rows[c][ch.row0 + t];
                 const int o = sol_index(s, r);
                 put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
                 put_i(sec.xidx, t, o);
@@ -387,9 +516,9 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             sp[0] = static_cast<int>(base / 16);  // CTA-relative for now
             sp[1] = round_up(sec.end, 16);
             sp[2] = region;
-            sp[3] = ch.r0;
+            sp[3] = static_cast<int>(wpos);
             sp[4] = wave_b_area(m);
-            sp[5] = round_up(8 * (m + (ch.r0 & 1)), 16);
+            sp[5] = round_up(8 * (m + static_cast<int>(wpos & 1)), 16);
         }
     }
     for (int c = 0; c < C; ++c)

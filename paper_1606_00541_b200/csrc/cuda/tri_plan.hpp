@@ -53,12 +53,18 @@ struct LevelLayout {
 LevelLayout build_levels(const TriSource& s);
 
 // ------------------------------------------------------------------ WAVE ----
-// Persistent wavefront kernel (one CTA per SM). CTA c owns the lower-frame
-// rows [c*per, (c+1)*per); inside the CTA, solver warp w owns the sub-range
-// [w*per_w, (w+1)*per_w). The CTA's rows of one level form a "chunk" (split
-// when large); because a level is sorted by lower-frame index
-// (reference level_schedule.cpp:51-56) a chunk is one contiguous reordered
-// range and each warp's rows in it are one contiguous segment.
+// Persistent wavefront kernel (one CTA per SM, cooperative launch so every
+// CTA is resident). Row ownership, in the lower frame:
+//  * default: CTA c owns rows [c*per, (c+1)*per) ("slabs"), solver warp w a
+//    contiguous sub-range of those;
+//  * when the factor is recognised as a structured nx x ny x nz grid in natural
+//    order (its dependency offsets are {1, nx, nx*ny} or the 27-point set),
+//    CTA (px, py) owns the z-pencil of an x-y tile and warp w a 2-D sub-tile of
+//    it. A wavefront then crosses ~sqrt(C) CTA boundaries per direction instead
+//    of C, and every level keeps all warps of an active CTA busy.
+// The CTA's rows of one level form a "chunk" (ordered by warp, then by row, and
+// split so that no warp has more than 32 rows); rows are numbered in "wave
+// order" (CTA, chunk, row) and the right-hand side is permuted into that order.
 //
 // Synchronisation replaces the reference's per-level barrier
 // (triangular.cpp:128) by dataflow:
@@ -105,6 +111,7 @@ struct WaveConfig {
     int lead = 4;             // a warp starts chunk j only after every warp finished chunk j-lead
     int max_bytes = 40960;    // chunk split: shared-memory region bytes
     int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
+    bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
 };
 
 struct WaveLayout {
@@ -114,6 +121,8 @@ struct WaveLayout {
     int max_width = 0;                    // sliced-ELL width W of every chunk
     long long exports = 0;                // mailboxes
     bool has_out = false;
+    bool pencils = false;                 // CTAs own z-pencils of a detected nx x ny x nz grid
+    int grid_nx = 0, grid_ny = 0;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
     std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region bytes, r0,
                                           //              b area bytes, b copy bytes, 0, 0
