@@ -68,6 +68,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         cfg.ctas = opt.ctas > 0 ? std::min(opt.ctas, sm_count()) : sm_count();  // one resident CTA per SM
         cfg.warps = kWaveSolverWarps;
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
+        if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
         cfg.warp_rows = 32;  // one row per lane
         const int budget = smem_optin() - 1024;  // static shared + slack
         plan::WaveLayout P;
@@ -229,6 +230,7 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
     a.ring_off = p_ring_off_;
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;
+    a.spin_ns = spin_ns_;
     a.trace = trace;
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)

@@ -368,16 +368,30 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
         double* const xs = a.xs;
         double* const outv = a.out;
         unsigned long long* const mbox = a.mbox;
+        double pend_x = 0.0;
+        int pend_xi = -1, pend_o = -1;
+        // TRACE: SM-clock breakdown of one chunk for solver warps 0 and 5 (trace words 48..63)
+        const int cw = (w == 5) ? 56 : -1;
+        long long c_top = 0;
+#define HEC_STAMP(K, DEP)                                                        \
+    if (TRACE && cw >= 0 && lane == 0) {                                           \
+        asm volatile("" ::"r"(static_cast<int>(DEP)) : "memory");                 \
+        tr(j, cw + (K)) = static_cast<unsigned long long>(clock64() - c_top);      \
+    }
         for (int j = 0; j < nch; ++j) {
             const int s = j & (NS - 1);
+            if (TRACE) c_top = clock64();
             mbar_wait(&bar_full[s], (j >> LG) & 1);  // blob and b landed
+            HEC_STAMP(0, 0)
             if (TRACE && lane == 0) tr(j, 8 + 3 * w) = gtimer();
             const unsigned char* blob = buf + boff[s];
             const int4 h0 = *reinterpret_cast<const int4*>(blob);  // m, mp, q0, flags
             const uint2 sg = *reinterpret_cast<const uint2*>(blob + kSeg + 8 * w);
             const int t0 = static_cast<int>(sg.x & 0xffffu), t1 = static_cast<int>(sg.x >> 16);
+            HEC_STAMP(1, t0 + h0.x)
             if (h0.w & 16)  // values from lower CTAs staged by the waiters
                 while (ld_volatile_u32(&hready[s]) != static_cast<uint32_t>(j + 1)) {
+                    if (a.spin_ns) __nanosleep(a.spin_ns);
                 }
             // the warps this segment reads from must have finished chunk j-1, and every
             // warp chunk j-lead (no warp runs further ahead: ring safety, tri_plan.hpp)
@@ -385,10 +399,12 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 const uint32_t need = ((sg.y >> lane) & 1u) ? static_cast<uint32_t>(j)
                                                             : static_cast<uint32_t>(max(0, j - L + 1));
                 while (ld_volatile_u32(&prog[lane]) < need) {
+                    if (a.spin_ns) __nanosleep(a.spin_ns);
                 }
             }
             __syncwarp();
             if (TRACE && lane == 0) tr(j, 9 + 3 * w) = gtimer();
+            HEC_STAMP(2, 0)
             if (t1 > t0) {
                 const int mp = h0.y, q0 = h0.z, flags = h0.w;
                 const double* dg = reinterpret_cast<const double*>(blob + kDiag);
@@ -415,11 +431,15 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                     }
 #pragma unroll
                     for (int u = 0; u < W; ++u) xv[u] = (dd[u] <= R ? ring : hb)[dd[u]];
+                    HEC_STAMP(3, dd[0] + static_cast<int>(vv[0]))
+                    HEC_STAMP(4, static_cast<int>(xv[0]))
                     const double y = __drcp_rn(dv);  // off the critical path
                     double acc = bst[t];
 #pragma unroll
                     for (int u = 0; u < W; ++u) acc = __dsub_rn(acc, __dmul_rn(vv[u], xv[u]));
+                    HEC_STAMP(5, static_cast<int>(acc))
                     x = div_rn(acc, dv, y);
+                    HEC_STAMP(6, static_cast<int>(x))
                 } else {
                     const double y = __drcp_rn(dv);
                     double acc = bst[t];
@@ -440,14 +460,10 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 }
                 // consumers in other CTAs are on the critical path: feed them first
                 if (act && e >= 0) mail_store(mbox + 2 * static_cast<size_t>(e), x, ep);
-                if (act) {
-                    ring[(q0 + t) & (R - 1)] = x;
-                    xs[xi] = x;
-                    if (flags & 2) {
-                        const int o = exl[mp + t];
-                        if (o >= 0) outv[o] = x;
-                    }
-                }
+                if (act) ring[(q0 + t) & (R - 1)] = x;
+                pend_x = x;
+                pend_xi = act ? xi : -1;
+                pend_o = (act && (flags & 2)) ? exl[mp + t] : -1;
             }
             __syncwarp();
             asm volatile("fence.acq_rel.cta;" ::: "memory");
@@ -456,9 +472,19 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 mbar_arrive(&bar_empty[s]);
                 if (TRACE) tr(j, 10 + 3 * w) = gtimer();
             }
+            HEC_STAMP(7, 0)
+            // the scattered stores of x leave the critical path: they are issued after
+            // the warp published its rows (only the own CTA reads x back, and only rows
+            // of chunks <= j-2, whose stores precede a later publication)
+            if (pend_xi >= 0) {
+                xs[pend_xi] = pend_x;
+                if (pend_o >= 0) outv[pend_o] = pend_x;
+                pend_xi = -1;
+            }
         }
     }
 
+#undef HEC_STAMP
     __syncthreads();
     if (tid == 0) {
         __threadfence();
