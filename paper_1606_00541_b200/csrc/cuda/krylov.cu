@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdint>
 #include <cmath>
 #include <vector>
 
@@ -36,8 +37,10 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return v;
 }
 
-// Finishes a reduction: block partial -> partials[bid]; last block sums them in
-// index order into *out (optionally sqrt'ed into *out_sqrt).
+// Finishes a reduction: block partial -> partials[bid]; the last block to
+// arrive sums them with a fixed-shape tree (thread t takes partials t, t+T, ..
+// in order, then block_sum) into *out (optionally sqrt'ed into *out_sqrt).
+// Fixed grid -> run-to-run reproducible.
 __device__ __forceinline__ void finish(double part, double* partials, unsigned* counter, double* out,
                                        double* out_sqrt) {
     __shared__ double sh[32];
@@ -49,29 +52,58 @@ __device__ __forceinline__ void finish(double part, double* partials, unsigned* 
         last = atomicAdd(counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
         __threadfence();
         double t = 0.0;
-        for (unsigned k = 0; k < gridDim.x; ++k) t = __dadd_rn(t, *((volatile double*)&partials[k]));
-        *out = t;
-        if (out_sqrt) *out_sqrt = __dsqrt_rn(t);
-        *counter = 0;
+        for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) t = __dadd_rn(t, __ldcg(&partials[k]));
+        __syncthreads();  // sh reuse
+        t = block_sum(t, sh);
+        if (threadIdx.x == 0) {
+            *out = t;
+            if (out_sqrt) *out_sqrt = __dsqrt_rn(t);
+            *counter = 0;
+        }
     }
 }
 
 // w -= (*h_prev) * v_prev  (if v_prev), then *out = dot(w, v_next).
-__global__ void k_mgs_step(int n, double* w, const double* v_prev, const double* h_prev,
-                           const double* v_next, double* partials, unsigned* counter, double* out,
-                           double* out_sqrt) {
+// Two elements per thread per step (16-byte loads when every vector is
+// 16-byte aligned), grid-stride; memory-bound.
+__global__ void __launch_bounds__(kThreads) k_mgs_step(int n, double* w, const double* v_prev, const double* h_prev,
+                                                     const double* v_next, double* partials, unsigned* counter,
+                                                     double* out, double* out_sqrt) {
     double acc = 0.0;
     const double h = v_prev ? *h_prev : 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const bool self = v_next == w;
+    const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(v_prev) |
+                       reinterpret_cast<uintptr_t>(v_next)) & 15) == 0;
+    const int stride = gridDim.x * blockDim.x;
+    int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (vec) {
+        const int n2 = n >> 1;
+        double2* w2 = reinterpret_cast<double2*>(w);
+        for (int i = i0; i < n2; i += stride) {
+            double2 wi = w2[i];
+            if (v_prev) {
+                const double2 vp = __ldg(reinterpret_cast<const double2*>(v_prev) + i);
+                wi.x = __dsub_rn(wi.x, __dmul_rn(h, vp.x));
+                wi.y = __dsub_rn(wi.y, __dmul_rn(h, vp.y));
+                w2[i] = wi;
+            }
+            const double2 vn = self ? wi : __ldg(reinterpret_cast<const double2*>(v_next) + i);
+            acc = __dadd_rn(acc, __dmul_rn(wi.x, vn.x));
+            acc = __dadd_rn(acc, __dmul_rn(wi.y, vn.y));
+        }
+        // an odd last element is left to the first thread of the grid
+        i0 = (blockIdx.x == 0 && threadIdx.x == 0) ? 2 * n2 : n;
+    }
+    for (int i = i0; i < n; i += stride) {
         double wi = w[i];
         if (v_prev) {
             wi = __dsub_rn(wi, __dmul_rn(h, v_prev[i]));
             w[i] = wi;
         }
-        const double vn = v_next == w ? wi : v_next[i];
+        const double vn = self ? wi : v_next[i];
         acc = __dadd_rn(acc, __dmul_rn(wi, vn));
     }
     finish(acc, partials, counter, out, out_sqrt);
@@ -107,7 +139,7 @@ KrylovOps::KrylovOps(int n) : n_(n) {
     int dev = 0, sms = 0;
     HEC_CUDA(cudaGetDevice(&dev));
     HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    grid_ = std::max(1, std::min(2 * sms, (n + kThreads - 1) / kThreads));
+    grid_ = std::max(1, std::min(4 * sms, (n + 2 * kThreads - 1) / (2 * kThreads)));
     HEC_CUDA(cudaMalloc(reinterpret_cast<void**>(&partials_), sizeof(double) * grid_));
     HEC_CUDA(cudaMalloc(reinterpret_cast<void**>(&counter_), sizeof(unsigned)));
     HEC_CUDA(cudaMemset(counter_, 0, sizeof(unsigned)));
@@ -166,8 +198,8 @@ GmresOutcome gmres_device(const DeviceSpmv& A, DevicePrecond* M, const double* b
     int dev = 0, sms = 0;
     HEC_CUDA(cudaGetDevice(&dev));
     HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = std::max(1, std::min(2 * sms, (n + kThreads - 1) / kThreads));
-    const size_t ldv = static_cast<size_t>(std::max(n, 1));
+    const int grid = std::max(1, std::min(4 * sms, (n + 2 * kThreads - 1) / (2 * kThreads)));
+    const size_t ldv = static_cast<size_t>((std::max(n, 1) + 3) / 4 * 4);  // 32-byte aligned basis columns
 
     DevBuf<double> V((mr + 1) * ldv), w(ldv), z(ldv), r(ldv), x(ldv), b(ldv), yv(mr + 1);
     DevBuf<double> hcol(mr + 3), partials(grid), scal(2);

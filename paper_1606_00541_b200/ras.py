@@ -261,7 +261,7 @@ def gmres(ops, comm, plan: RasPlan, b_own, restart: int = 20, max_iters: int = 1
         raise ValueError("gmres: invalid configuration")
     t0 = time.perf_counter()
     n, nl, mr = plan.n_own, plan.n_loc, restart
-    ldv = max(n, 1)
+    ldv = (max(n, 1) + 3) // 4 * 4  # 32-byte aligned basis columns (vectorised Krylov kernels)
     V = ops.vec((mr + 1) * ldv)
     b = ops.from_host(b_own)
     x, r = ops.vec(n), ops.vec(n)

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--restart", type=int, default=30)
     ap.add_argument("--overlap", type=int, default=1)
     ap.add_argument("--backend", default="nccl")
+    ap.add_argument("--max-iters", type=int, default=10000)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -35,7 +36,7 @@ def main():
     t0 = time.time()
     a = H.gen_poisson7(s, s, s)
     b = H.spmv_csr(a, np.ones(a.n_rows), workers=os.cpu_count())
-    solver = ras.RasGmres(a, overlap=args.overlap, restart=args.restart)
+    solver = ras.RasGmres(a, overlap=args.overlap, restart=args.restart, max_iters=args.max_iters)
     t_setup = time.time() - t0
     solver.solve(b)  # warm-up (device layouts, workspaces)
     torch.cuda.synchronize()
