@@ -67,9 +67,17 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         plan::WaveConfig cfg;
         cfg.ctas = opt.ctas > 0 ? std::min(opt.ctas, sm_count()) : sm_count();  // one resident CTA per SM
         cfg.warps = kWaveSolverWarps;
+        cfg.warp_rows = 32;  // one row per lane
+        if (const char* e = std::getenv("HEC_WAVE_RPL")) {  // layout knob: 1 = 16 warps, 2/4/8 = 1 warp x rpl rows/lane
+            const int rpl = std::atoi(e);
+            cfg.auto_warps = false;
+            if (rpl >= 2) {
+                cfg.warps = 1;
+                cfg.warp_rows = 32 * (rpl >= 8 ? 8 : (rpl >= 4 ? 4 : 2));
+            }
+        }
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
-        cfg.warp_rows = 32;  // one row per lane
         const int budget = smem_optin() - 1024;  // static shared + slack
         plan::WaveLayout P;
         bool ok = true;
@@ -87,15 +95,16 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_inflight_ = P.inflight;
             p_lead_ = P.lead;
             if (std::getenv("HEC_DEBUG"))
-                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d W=%d %s grid=%dx%d max_region=%d "
+                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d rpl=%d W=%d %s grid=%dx%d max_region=%d "
                              "buf=%d exports=%lld deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n,
-                             P.chunks, P.ctas, P.warps, P.max_width, P.pencils ? "pencils" : "slabs", P.grid_nx,
+                             P.chunks, P.ctas, P.warps, P.warps > 1 ? 1 : std::max(2, P.rpl), P.max_width, P.pencils ? "pencils" : (P.strips ? "strips" : "slabs"), P.grid_nx,
                              P.grid_ny, P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps,
                              P.halo_deps, P.halo_values);
             p_smem_ = p_buf_off_ + p_buf_bytes_;
             p_ctas_ = P.ctas;
-            p_kernel_ = wave_kernel(P.max_width, false);
-            p_kernel_trace_ = wave_kernel(P.max_width, true);
+            p_rpl_ = P.warps > 1 ? 1 : std::max(2, P.rpl > 1 ? P.rpl : cfg.warp_rows / 32);
+            p_kernel_ = wave_kernel(P.max_width, P.warps, p_rpl_, false);
+            p_kernel_trace_ = wave_kernel(P.max_width, P.warps, p_rpl_, true);
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_trace_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
             p_exports_ = P.exports;
@@ -106,6 +115,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_cta0_host_ = P.cta_chunk0;
             stats_.ctas = p_ctas_;
             stats_.threads = kWaveRoleThreads + 32 * p_warps_;
+            if (!p_kernel_) throw std::invalid_argument("hec_tri_create: no wave kernel for this width");
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
             stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size() +

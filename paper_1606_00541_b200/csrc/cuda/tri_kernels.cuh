@@ -49,8 +49,10 @@ struct WaveArgs {
 };
 
 void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
-// kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise)
-void* wave_kernel(int width, bool trace);
+// kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise):
+// 16 solver warps with one row per lane, or one solver warp with rpl (2, 4, 8)
+// rows per lane
+void* wave_kernel(int width, int warps, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;

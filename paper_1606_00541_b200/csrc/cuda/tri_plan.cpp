@@ -197,7 +197,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     WaveLayout P;
     const int n = s.n;
     const int C0 = std::max(1, std::min(cfg.ctas, std::max(n, 1)));
-    const int NW = std::max(1, std::min(cfg.warps, 32));
+    int NW = std::max(1, std::min(cfg.warps, 32));
+    int warp_rows = cfg.warp_rows;
     const int R = cfg.ring;
     P.n = n;
     P.nlev = s.nlev;
@@ -234,10 +235,35 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
         use_pencils = max_levels_per_cta(owner_i, C_used) < max_levels_per_cta(slab, C0);
     }
+    // strips: when the row index follows the levels (e.g. an RCM ordering), index
+    // slabs would give each CTA only a handful of consecutive levels and the CTAs
+    // would run one after another; then every CTA takes a fraction of every level
+    bool use_strips = false;
+    if (!use_pencils && cfg.strips) {
+        const int per = (n + C0 - 1) / C0;
+        std::vector<int> slab(n);
+        for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
+        use_strips = s.nlev >= 16 && static_cast<long long>(max_levels_per_cta(slab, C0)) * 8 < s.nlev;
+    }
     if (use_pencils) {
         P.pencils = true;
         P.grid_nx = geo.nx;
         P.grid_ny = geo.ny;
+    } else if (use_strips) {
+        P.strips = true;
+        for (int k = 0; k < s.nlev; ++k) {
+            const int r0 = s.level_starts[k], mk = s.level_starts[k + 1] - r0;
+            for (int c = 0; c < C0; ++c) {
+                const int a0 = static_cast<int>(static_cast<long long>(mk) * c / C0);
+                const int a1 = static_cast<int>(static_cast<long long>(mk) * (c + 1) / C0);
+                const int pw = std::max(1, (a1 - a0 + NW - 1) / NW);
+                for (int q = a0; q < a1; ++q) {
+                    owner_i[s.inv_perm[r0 + q]] = c;
+                    warp_i[s.inv_perm[r0 + q]] = std::min((q - a0) / pw, NW - 1);
+                }
+            }
+        }
+        C_used = C0;
     } else {
         // slabs: CTA c owns [c*per, (c+1)*per), warps contiguous sub-ranges
         const int per = n > 0 ? (n + C0 - 1) / C0 : 1;
@@ -251,6 +277,26 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     P.ctas = C_used;
     const int C = C_used;
+
+    // one solver warp with two rows per lane when no CTA ever has more than 64
+    // rows in a level (e.g. 27-point slabs): no warp-to-warp synchronisation at all
+    P.rpl = 1;
+    if (cfg.auto_warps && !P.pencils && NW > 1 && n > 0) {
+        std::vector<int> lev_cnt(static_cast<std::size_t>(C), 0);
+        int worst = 0;
+        for (int k = 0; k < s.nlev && worst <= 64; ++k) {
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r)
+                worst = std::max(worst, ++lev_cnt[owner_i[s.inv_perm[r]]]);
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) lev_cnt[owner_i[s.inv_perm[r]]] = 0;
+        }
+        if (worst <= 64) {
+            NW = 1;
+            P.rpl = 2;
+            warp_rows = 64;
+            std::fill(warp_i.begin(), warp_i.end(), 0);
+        }
+    }
+    P.warps = NW;
 
     std::vector<int> cnt(n), owner_r(n), warp_r(n), nforeign(n, 0);
 #pragma omp parallel for schedule(static)
@@ -324,7 +370,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                         const int wcnt = warp_r[r] == cur_w ? cur_cnt + 1 : 1;
                         const int bytes =
                             wave_region_bytes(ch.m + 1, h2, wave_sections(ch.m + 1, W, NW, h2, t2, fl).end);
-                        if (ch.m > 0 && (wcnt > cfg.warp_rows || bytes > cfg.max_bytes)) break;
+                        if (ch.m > 0 && (wcnt > warp_rows || bytes > cfg.max_bytes)) break;
                         cur_w = warp_r[r];
                         cur_cnt = wcnt;
                         ch.ntail = t2;

@@ -57,6 +57,9 @@ LevelLayout build_levels(const TriSource& s);
 // CTA is resident). Row ownership, in the lower frame:
 //  * default: CTA c owns rows [c*per, (c+1)*per) ("slabs"), solver warp w a
 //    contiguous sub-range of those;
+//  * when the row index follows the levels (an RCM-like ordering), slabs would
+//    hand each CTA a few consecutive levels only: then "strips" -- each CTA
+//    owns the c-th fraction of every level;
 //  * when the factor is recognised as a structured nx x ny x nz grid in natural
 //    order (its dependency offsets are {1, nx, nx*ny} or the 27-point set),
 //    CTA (px, py) owns the z-pencil of an x-y tile and warp w a 2-D sub-tile of
@@ -105,23 +108,26 @@ LevelLayout build_levels(const TriSource& s);
 struct WaveConfig {
     int ctas = 148;
     int warps = 8;            // solver warps per CTA (<= 32)
-    int warp_rows = 64;       // max rows of one warp in one chunk (32 * rows per lane)
+    int warp_rows = 32;       // max rows of one warp in one chunk (32 * rows per lane)
+    bool auto_warps = true;   // one solver warp (2 rows per lane) when every CTA level has <= 64 rows
     int ring = 8192;          // x ring entries (power of two); slot `ring` holds 0.0
     int inflight = 16;        // max chunks in flight per CTA (descriptor slots)
     int lead = 4;             // a warp starts chunk j only after every warp finished chunk j-lead
     int max_bytes = 40960;    // chunk split: shared-memory region bytes
     int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
     bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
+    bool strips = true;       // row index follows the levels: every CTA takes a fraction of each level
 };
 
 struct WaveLayout {
-    int n = 0, nlev = 0, ctas = 0, warps = 0, ring = 0, inflight = 0, lead = 0;
+    int n = 0, nlev = 0, ctas = 0, warps = 0, rpl = 1, ring = 0, inflight = 0, lead = 0;
     int chunks = 0;
     int max_region = 0;                   // bytes of the largest chunk region
     int max_width = 0;                    // sliced-ELL width W of every chunk
     long long exports = 0;                // mailboxes
     bool has_out = false;
     bool pencils = false;                 // CTAs own z-pencils of a detected nx x ny x nz grid
+    bool strips = false;                  // every CTA owns a fraction of every level
     int grid_nx = 0, grid_ny = 0;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
     std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region bytes, r0,

@@ -221,10 +221,10 @@ __device__ __forceinline__ double accumulate(double acc, const int* dep, const d
 // Shared-memory control block (kWaveCtrlBytes): prog[32] | hready[32] (+pad)
 // | roff[32] | bar_full[32] | bar_empty[32] | (unused) | boff[32] | ticket.
 // roff = region start (producer), boff = blob start.
-template <int W, int NW, bool TRACE>
+template <int W, int NW, int RPL, bool TRACE>
 __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs a) {
     constexpr int kSeg = plan::kWaveHeaderBytes;
-    constexpr int kDiag = kSeg + 8 * NW;  // 16-byte multiple
+    constexpr int kDiag = kSeg + (8 * NW + 15) / 16 * 16;  // seg table rounded to 16 bytes (tri_plan.hpp)
     extern __shared__ __align__(128) unsigned char smem[];
     uint32_t* prog = reinterpret_cast<uint32_t*>(smem);
     uint32_t* hready = reinterpret_cast<uint32_t*>(smem + 128);
@@ -368,8 +368,13 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
         double* const xs = a.xs;
         double* const outv = a.out;
         unsigned long long* const mbox = a.mbox;
-        double pend_x = 0.0;
-        int pend_xi = -1, pend_o = -1;
+        double pend_x[RPL];
+        int pend_xi[RPL], pend_o[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) {
+            pend_x[k] = 0.0;
+            pend_xi[k] = pend_o[k] = -1;
+        }
         // TRACE: SM-clock breakdown of one chunk for solver warps 0 and 5 (trace words 48..63)
         const int cw = (w == 5) ? 56 : -1;
         long long c_top = 0;
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 }
             // the warps this segment reads from must have finished chunk j-1, and every
             // warp chunk j-lead (no warp runs further ahead: ring safety, tri_plan.hpp)
-            if (lane < NW) {
+            if (NW > 1 && lane < NW) {
                 const uint32_t need = ((sg.y >> lane) & 1u) ? static_cast<uint32_t>(j)
                                                             : static_cast<uint32_t>(max(0, j - L + 1));
                 while (ld_volatile_u32(&prog[lane]) < need) {
@@ -414,61 +419,92 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
                 const int* exl = xidx + mp;
                 const double* bst = reinterpret_cast<const double*>(blob) - ((h0.x + 4) & ~3) + ((flags >> 5) & 1);
                 const double* hb = reinterpret_cast<const double*>(blob + reinterpret_cast<const int*>(blob)[7]) - (R + 1);
-                // one row per lane (the layout splits chunks so a warp never has more than 32)
-                const bool act = t0 + lane < t1;
-                const int t = act ? t0 + lane : t0;
-                const double dv = dg[t];
-                const int e = exl[t], xi = xidx[t];
-                double x;
+                // RPL rows per lane (the layout splits chunks so a warp never has more than
+                // 32 * RPL rows), processed together for instruction-level parallelism
+                bool act[RPL];
+                int tt[RPL], ee[RPL];
+                double xx[RPL];
+#pragma unroll
+                for (int k = 0; k < RPL; ++k) {
+                    act[k] = t0 + lane + 32 * k < t1;
+                    tt[k] = act[k] ? t0 + lane + 32 * k : t0;
+                }
                 if ((flags & 9) == 0) {
                     // fast path: every dependency in shared memory, no tail
-                    int dd[W];
-                    double vv[W], xv[W];
+                    int dd[RPL][W];
+                    double vv[RPL][W], xv[RPL][W], dv[RPL], acc[RPL];
+                    // row groups past the segment end are skipped (warp-uniform test)
 #pragma unroll
-                    for (int u = 0; u < W; ++u) {
-                        dd[u] = dep[u * mp + t];
-                        vv[u] = val[u * mp + t];
+                    for (int k = 0; k < RPL; ++k) {
+                        if (k > 0 && t0 + 32 * k >= t1) break;
+                        dv[k] = dg[tt[k]];
+                        acc[k] = bst[tt[k]];
+                        ee[k] = exl[tt[k]];
+#pragma unroll
+                        for (int u = 0; u < W; ++u) {
+                            dd[k][u] = dep[u * mp + tt[k]];
+                            vv[k][u] = val[u * mp + tt[k]];
+                        }
                     }
 #pragma unroll
-                    for (int u = 0; u < W; ++u) xv[u] = (dd[u] <= R ? ring : hb)[dd[u]];
-                    HEC_STAMP(3, dd[0] + static_cast<int>(vv[0]))
-                    HEC_STAMP(4, static_cast<int>(xv[0]))
-                    const double y = __drcp_rn(dv);  // off the critical path
-                    double acc = bst[t];
+                    for (int k = 0; k < RPL; ++k) {
+                        if (k > 0 && t0 + 32 * k >= t1) break;
 #pragma unroll
-                    for (int u = 0; u < W; ++u) acc = __dsub_rn(acc, __dmul_rn(vv[u], xv[u]));
-                    HEC_STAMP(5, static_cast<int>(acc))
-                    x = div_rn(acc, dv, y);
-                    HEC_STAMP(6, static_cast<int>(x))
+                        for (int u = 0; u < W; ++u) xv[k][u] = (dd[k][u] <= R ? ring : hb)[dd[k][u]];
+                    }
+                    HEC_STAMP(3, dd[0][0])
+                    HEC_STAMP(4, static_cast<int>(xv[0][0]))
+#pragma unroll
+                    for (int k = 0; k < RPL; ++k) {
+                        if (k > 0 && t0 + 32 * k >= t1) {
+                            xx[k] = 0.0;
+                            ee[k] = -1;
+                            continue;
+                        }
+                        const double y = __drcp_rn(dv[k]);  // off the critical path
+#pragma unroll
+                        for (int u = 0; u < W; ++u) acc[k] = __dsub_rn(acc[k], __dmul_rn(vv[k][u], xv[k][u]));
+                        xx[k] = div_rn(acc[k], dv[k], y);
+                    }
+                    HEC_STAMP(6, static_cast<int>(xx[0]))
                 } else {
-                    const double y = __drcp_rn(dv);
-                    double acc = bst[t];
                     const uint32_t ring_s = smem_u32(ring), hb_s = smem_u32(hb);
 #pragma unroll
-                    for (int u = 0; u < W; ++u)
-                        acc = __dsub_rn(acc, __dmul_rn(val[u * mp + t], dep_value(dep[u * mp + t], R, ring_s, hb_s, xs)));
-                    if (flags & 1) {  // CSR tail beyond the sliced-ELL width, storage order
-                        const int* tptr = reinterpret_cast<const int*>(blob + reinterpret_cast<const int*>(blob)[6]);
-                        const int mt = (mp + 4) & ~3;  // round_up(mp + 1, 4)
-                        const int ntl = tptr[mp];
-                        const double* tval = reinterpret_cast<const double*>(tptr + mt);
-                        const int* tdep = reinterpret_cast<const int*>(tval + ((ntl + 1) & ~1));
-                        for (int k = tptr[t]; k < tptr[t + 1]; ++k)
-                            acc = __dsub_rn(acc, __dmul_rn(tval[k], dep_value(tdep[k], R, ring_s, hb_s, xs)));
+                    for (int k = 0; k < RPL; ++k) {
+                        const int t = tt[k];
+                        const double dv = dg[t];
+                        ee[k] = exl[t];
+                        const double y = __drcp_rn(dv);
+                        double acc = bst[t];
+#pragma unroll
+                        for (int u = 0; u < W; ++u)
+                            acc = __dsub_rn(acc, __dmul_rn(val[u * mp + t], dep_value(dep[u * mp + t], R, ring_s, hb_s, xs)));
+                        if (flags & 1) {  // CSR tail beyond the sliced-ELL width, storage order
+                            const int* tptr = reinterpret_cast<const int*>(blob + reinterpret_cast<const int*>(blob)[6]);
+                            const int mt = (mp + 4) & ~3;  // round_up(mp + 1, 4)
+                            const int ntl = tptr[mp];
+                            const double* tval = reinterpret_cast<const double*>(tptr + mt);
+                            const int* tdep = reinterpret_cast<const int*>(tval + ((ntl + 1) & ~1));
+                            for (int e = tptr[t]; e < tptr[t + 1]; ++e)
+                                acc = __dsub_rn(acc, __dmul_rn(tval[e], dep_value(tdep[e], R, ring_s, hb_s, xs)));
+                        }
+                        xx[k] = div_rn(acc, dv, y);
                     }
-                    x = div_rn(acc, dv, y);
                 }
-                // consumers in other CTAs are on the critical path: feed them first
-                if (act && e >= 0) mail_store(mbox + 2 * static_cast<size_t>(e), x, ep);
-                if (act) ring[(q0 + t) & (R - 1)] = x;
-                pend_x = x;
-                pend_xi = act ? xi : -1;
-                pend_o = (act && (flags & 2)) ? exl[mp + t] : -1;
+#pragma unroll
+                for (int k = 0; k < RPL; ++k) {
+                    // consumers in other CTAs are on the critical path: feed them first
+                    if (act[k] && ee[k] >= 0) mail_store(mbox + 2 * static_cast<size_t>(ee[k]), xx[k], ep);
+                    if (act[k]) ring[(q0 + tt[k]) & (R - 1)] = xx[k];
+                    pend_x[k] = xx[k];
+                    pend_xi[k] = act[k] ? xidx[tt[k]] : -1;
+                    pend_o[k] = (act[k] && (flags & 2)) ? exl[mp + tt[k]] : -1;
+                }
             }
             __syncwarp();
-            asm volatile("fence.acq_rel.cta;" ::: "memory");
+            if (NW > 1) asm volatile("fence.acq_rel.cta;" ::: "memory");  // ring rows -> other warps
             if (lane == 0) {
-                st_volatile_u32(&prog[w], static_cast<uint32_t>(j + 1));
+                if (NW > 1) st_volatile_u32(&prog[w], static_cast<uint32_t>(j + 1));
                 mbar_arrive(&bar_empty[s]);
                 if (TRACE) tr(j, 10 + 3 * w) = gtimer();
             }
@@ -476,11 +512,13 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
             // the scattered stores of x leave the critical path: they are issued after
             // the warp published its rows (only the own CTA reads x back, and only rows
             // of chunks <= j-2, whose stores precede a later publication)
-            if (pend_xi >= 0) {
-                xs[pend_xi] = pend_x;
-                if (pend_o >= 0) outv[pend_o] = pend_x;
-                pend_xi = -1;
-            }
+#pragma unroll
+            for (int k = 0; k < RPL; ++k)
+                if (pend_xi[k] >= 0) {
+                    xs[pend_xi[k]] = pend_x[k];
+                    if (pend_o[k] >= 0) outv[pend_o[k]] = pend_x[k];
+                    pend_xi[k] = -1;
+                }
         }
     }
 
@@ -512,24 +550,31 @@ void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_
     k_permute_in<<<blocks, 256, 0, st>>>(b, bidx, bp, n);
 }
 
-#define HEC_WAVE_INST(WD)                                    \
-    template __global__ void k_wave<WD, 16, false>(WaveArgs); \
-    template __global__ void k_wave<WD, 16, true>(WaveArgs);
+// solver layouts: 16 warps x 1 row per lane, or 1 warp x RPL rows per lane
+#define HEC_WAVE_INST3(WD, NWW, RP)                                \
+    template __global__ void k_wave<WD, NWW, RP, false>(WaveArgs); \
+    template __global__ void k_wave<WD, NWW, RP, true>(WaveArgs);
+#define HEC_WAVE_INST(WD) HEC_WAVE_INST3(WD, 16, 1) HEC_WAVE_INST3(WD, 1, 2) HEC_WAVE_INST3(WD, 1, 4) \
+    HEC_WAVE_INST3(WD, 1, 8)
 HEC_WAVE_INST(1) HEC_WAVE_INST(2) HEC_WAVE_INST(3) HEC_WAVE_INST(4) HEC_WAVE_INST(5) HEC_WAVE_INST(6)
 HEC_WAVE_INST(7) HEC_WAVE_INST(8) HEC_WAVE_INST(10) HEC_WAVE_INST(13) HEC_WAVE_INST(16)
 #undef HEC_WAVE_INST
+#undef HEC_WAVE_INST3
 
-void* wave_kernel(int width, bool trace) {
-#define HEC_PICK(WD)                                                                   \
-    case WD:                                                                           \
-        return trace ? reinterpret_cast<void*>(&k_wave<WD, kWaveSolverWarps, true>)  \
-                     : reinterpret_cast<void*>(&k_wave<WD, kWaveSolverWarps, false>);
+void* wave_kernel(int width, int warps, int rpl, bool trace) {
+#define HEC_K(WD, NWW, RP) \
+    (trace ? reinterpret_cast<void*>(&k_wave<WD, NWW, RP, true>) : reinterpret_cast<void*>(&k_wave<WD, NWW, RP, false>))
+#define HEC_PICK(WD)                                                                                  \
+    case WD:                                                                                          \
+        if (warps > 1) return HEC_K(WD, 16, 1);                                                       \
+        return rpl >= 8 ? HEC_K(WD, 1, 8) : rpl >= 4 ? HEC_K(WD, 1, 4) : HEC_K(WD, 1, 2);
     switch (width) {
         HEC_PICK(1) HEC_PICK(2) HEC_PICK(3) HEC_PICK(4) HEC_PICK(5) HEC_PICK(6)
         HEC_PICK(7) HEC_PICK(8) HEC_PICK(10) HEC_PICK(13) HEC_PICK(16)
         default: return nullptr;
     }
 #undef HEC_PICK
+#undef HEC_K
 }
 
 }  // namespace hec::dev
