@@ -197,3 +197,30 @@ def test_wave_width_classes_and_splits(H, orc):
                 got, info = device_solve(H, p, b, 2, ctas=int(rng.integers(1, 40)))
                 assert info["strategy"] == 2
                 assert bits_equal(got, want), (w, upper)
+
+
+@pytest.mark.parametrize("knobs", [{}, {"HEC_WAVE_SLABS": "1"}, {"HEC_WAVE_RPL": "1"}, {"HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_RPL": "4"}, {"HEC_WAVE_RPL": "8"}])
+def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
+    # every row-ownership layout (z-pencils, slabs, strips) and solver shape
+    # (16 warps x 1 row, 1 warp x 2/4/8 rows) gives the reference's bits
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(23)
+    cases = [("natural 7pt", H.gen_poisson7(28, 26, 24), None),          # pencils
+             ("natural 27pt", H.gen_poisson27(18, 17, 16), None),       # slabs, 1 warp
+             ("rcm 7pt", H.gen_poisson7(24, 22, 20), "rcm"),            # strips
+             ("random 7pt", H.gen_poisson7(20, 18, 16), "random")]      # slabs
+    for name, a, order in cases:
+        if order == "rcm":
+            a = H.permute_symmetric(a, H.rcm_ordering(a))
+        elif order == "random":
+            a = H.permute_symmetric(a, H.random_ordering(a.n_rows, 1606))
+        f = H.ilu0(a)
+        for fac, upper in ((f.l, False), (f.u, True)):
+            p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+            b = rng.uniform(-1, 1, a.n_rows)
+            want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+            got, info = device_solve(H, p, b, 2)
+            assert info["strategy"] == 2, name
+            assert bits_equal(got, want), (name, upper, knobs)
