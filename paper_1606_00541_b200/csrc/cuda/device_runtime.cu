@@ -161,8 +161,9 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
     auto& w = ws_[st];
     if (!w) {
         w = std::make_unique<Workspace>();
-        w->counters.alloc(2);
-        HEC_CUDA(cudaMemset(w->counters.p, 0, sizeof(uint32_t) * 2));
+        w->counters.alloc(3);  // ticket, CTAs finished, mailbox epoch (advanced by the kernel itself)
+        const uint32_t init[3] = {0u, 0u, 1u};
+        HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
         w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
         w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
         HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
@@ -218,10 +219,6 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
         return;
     }
     Workspace& w = workspace(st);
-    if (++w.epoch == 0) {  // 2^32 solves on this stream: clear the mailboxes and restart the epochs
-        HEC_CUDA(cudaMemsetAsync(w.mailbox.p, 0, sizeof(unsigned long long) * w.mailbox.count, st));
-        w.epoch = 1;
-    }
     WaveArgs a{};
     a.blobs = p_blob_.p;
     a.spans = reinterpret_cast<const int4*>(p_spans_.p);
@@ -231,7 +228,6 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
     a.out = has_out_ ? out : nullptr;
     a.mbox = w.mailbox.p;
     a.counters = w.counters.p;
-    a.epoch = w.epoch;
     a.ctas = p_ctas_;
     a.inflight = p_inflight_;
     a.inflight_log2 = __builtin_ctz(static_cast<unsigned>(p_inflight_));

@@ -95,10 +95,9 @@ public:
 
 private:
     struct Workspace {
-        DevBuf<uint32_t> counters;            // ticket + finished CTAs
+        DevBuf<uint32_t> counters;            // ticket, finished CTAs, mailbox epoch
         DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
         DevBuf<double> bp;                    // right-hand side in reordered-row order
-        uint32_t epoch = 0;                   // last solve's epoch on this stream
     };
     Workspace& workspace(cudaStream_t st);
     void run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st);

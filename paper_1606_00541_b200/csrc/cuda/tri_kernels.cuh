@@ -34,8 +34,8 @@ struct WaveArgs {
     double* xs;
     double* out;
     unsigned long long* mbox;    // 2 words per exported row: {lo32|epoch<<32, hi32|epoch<<32}
-    uint32_t* counters;          // [0] ticket, [1] CTAs finished
-    uint32_t epoch;              // this solve's mailbox epoch (never 0)
+    uint32_t* counters;          // [0] ticket, [1] CTAs finished, [2] this solve's mailbox epoch
+                                 // (advanced by the last CTA out: graph-replay safe)
     int ctas;
     int inflight;                // descriptor slots (power of two <= 32)
     int inflight_log2;

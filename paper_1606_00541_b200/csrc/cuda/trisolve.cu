@@ -127,6 +127,11 @@ void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, c
 // ------------------------------------------------------------------ WAVE ----
 using plan::WaveHeader;
 
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
     uint64_t* bar_empty = bar_full + 32;
     uint32_t* boff = reinterpret_cast<uint32_t*>(smem + 1280);
     int* s_cta = reinterpret_cast<int*>(smem + 1408);
+    __shared__ uint32_t s_epoch;
     double* ring = reinterpret_cast<double*>(smem + a.ring_off);
     unsigned char* buf = smem + a.buf_off;
     const int NS = a.inflight, LG = a.inflight_log2;
@@ -243,6 +249,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
     if (tid < 128) prog[tid] = 0u;  // prog, slot, roff
     if (tid == 0) {
         *s_cta = static_cast<int>(atomicAdd(&a.counters[0], 1u));
+        s_epoch = ld_relaxed_u32(&a.counters[2]);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&bar_full[s], 1);
             mbar_init(&bar_empty[s], NW);
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
     } else if (warp <= kWaveWaiters) {
         // ------------- waiters (round robin over chunks): stage the values this
         // chunk reads from lower CTAs, then publish it -------------
-        const uint32_t ep = a.epoch;
+        const uint32_t ep = s_epoch;
         for (int j = warp - 1; j < nch; j += kWaveWaiters) {
             const int s = j & (NS - 1);
             mbar_wait(&bar_full[s], (j >> LG) & 1);
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
     } else {
         // ------------- solvers: warp w owns a fixed slice of the CTA's rows -------------
         const int w = warp - 1 - kWaveWaiters;
-        const uint32_t ep = a.epoch;
+        const uint32_t ep = s_epoch;
         const uint32_t ring_s = smem_u32(ring);
         const int L = a.lead;
         double* const xs = a.xs;
@@ -528,9 +535,11 @@ __global__ void __launch_bounds__(kWaveRoleThreads + 32 * NW, 1) k_wave(WaveArgs
         __threadfence();
         const uint32_t finished = atomicAdd(&a.counters[1], 1u);
         if (finished == static_cast<uint32_t>(a.ctas) - 1) {
-            // last CTA out: re-arm the tickets for the next launch on this stream
+            // last CTA out: re-arm the tickets and advance the mailbox epoch for the
+            // next launch on this stream (never 0: 0 marks a mailbox never written)
             a.counters[0] = 0;
             a.counters[1] = 0;
+            a.counters[2] = s_epoch == 0xffffffffu ? 1u : s_epoch + 1u;
             __threadfence();
         }
     }

@@ -224,3 +224,32 @@ def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
             got, info = device_solve(H, p, b, 2)
             assert info["strategy"] == 2, name
             assert bits_equal(got, want), (name, upper, knobs)
+
+
+def test_cuda_graph_replay(H, orc):
+    # the mailbox epoch lives on the device (advanced by the kernel), so an
+    # L+U pair captured once in a CUDA graph replays with the reference's bits
+    torch = pytest.importorskip("torch")
+    a = H.gen_poisson7(30, 28, 26)
+    f = H.ilu0(a)
+    tl = H.DeviceTri.create(H.prepare_lower(f.l), strategy=2)
+    tu = H.DeviceTri.create(H.prepare_upper(f.u), strategy=2)
+    ol, ou = orc.prepare(to_oracle(f.l)), orc.prepare(to_oracle(f.u), upper=True)
+    s = torch.cuda.Stream()
+    bd = torch.zeros(a.n_rows, dtype=torch.float64, device="cuda")
+    y, x = torch.empty_like(bd), torch.empty_like(bd)
+    with torch.cuda.stream(s):
+        tl.solve(bd, y, stream=s)      # per-stream workspace allocated outside capture
+        tu.solve(y, x, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tl.solve(bd, y, stream=s)
+        tu.solve(y, x, stream=s)
+    rng = np.random.default_rng(29)
+    for rep in range(5):
+        b = rng.uniform(-1, 1, a.n_rows)
+        bd.copy_(torch.from_numpy(b))
+        g.replay()
+        torch.cuda.synchronize()
+        assert bits_equal(x.cpu().numpy(), orc.solve(ou, orc.solve(ol, b))), rep
