@@ -66,18 +66,18 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
     if (strategy_ == 2 && n_ > 0) {
         plan::WaveConfig cfg;
         cfg.ctas = opt.ctas > 0 ? std::min(opt.ctas, sm_count()) : sm_count();  // one resident CTA per SM
-        cfg.warps = kWaveSolverWarps;
-        cfg.warp_rows = 32;  // one row per lane
-        if (const char* e = std::getenv("HEC_WAVE_RPL")) {  // layout knob: 1 = 16 warps, 2/4/8 = 1 warp x rpl rows/lane
-            const int rpl = std::atoi(e);
-            cfg.auto_warps = false;
-            if (rpl >= 2) {
-                cfg.warps = 1;
-                cfg.warp_rows = 32 * (rpl >= 8 ? 8 : (rpl >= 4 ? 4 : 2));
-            }
+        // solver-shape knobs (default: chosen by the planner from the rows per CTA
+        // level): HEC_WAVE_G warps per chunk, HEC_WAVE_K groups, HEC_WAVE_RPL rows per lane
+        if (const char* e = std::getenv("HEC_WAVE_G")) {
+            cfg.group = std::atoi(e);
+            if (const char* k = std::getenv("HEC_WAVE_K")) cfg.groups = std::atoi(k);
+            if (const char* r = std::getenv("HEC_WAVE_RPL")) cfg.rpl = std::atoi(r);
+            if (!wave_kernel(1, cfg.group, cfg.groups, cfg.rpl, false))
+                throw std::invalid_argument("HEC_WAVE_G/K/RPL: no kernel for this solver shape");
         }
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
+        if (const char* e = std::getenv("HEC_WAVE_DBG")) dbg_ = std::atoi(e);               // experiments only
         const int budget = smem_optin() - 1024;  // static shared + slack
         plan::WaveLayout P;
         bool ok = true;
@@ -95,16 +95,17 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_inflight_ = P.inflight;
             p_lead_ = P.lead;
             if (std::getenv("HEC_DEBUG"))
-                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d rpl=%d W=%d %s grid=%dx%d max_region=%d "
+                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d (%dx%d) rpl=%d W=%d %s grid=%dx%d max_region=%d "
                              "buf=%d exports=%lld deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n,
-                             P.chunks, P.ctas, P.warps, P.warps > 1 ? 1 : std::max(2, P.rpl), P.max_width, P.pencils ? "pencils" : (P.strips ? "strips" : "slabs"), P.grid_nx,
+                             P.chunks, P.ctas, P.warps, P.group, P.groups, P.rpl, P.max_width, P.pencils ? "pencils" : (P.strips ? "strips" : "slabs"), P.grid_nx,
                              P.grid_ny, P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps,
                              P.halo_deps, P.halo_values);
             p_smem_ = p_buf_off_ + p_buf_bytes_;
             p_ctas_ = P.ctas;
-            p_rpl_ = P.warps > 1 ? 1 : std::max(2, P.rpl > 1 ? P.rpl : cfg.warp_rows / 32);
-            p_kernel_ = wave_kernel(P.max_width, P.warps, p_rpl_, false);
-            p_kernel_trace_ = wave_kernel(P.max_width, P.warps, p_rpl_, true);
+            p_rpl_ = P.rpl;
+            p_kernel_ = wave_kernel(P.max_width, P.group, P.groups, p_rpl_, false);
+            p_kernel_trace_ = wave_kernel(P.max_width, P.group, P.groups, p_rpl_, true);
+            if (!p_kernel_ || !p_kernel_trace_) throw std::runtime_error("hec: no wave kernel for this layout");
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
             HEC_CUDA(cudaFuncSetAttribute(p_kernel_trace_, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_));
             p_exports_ = P.exports;
@@ -237,6 +238,7 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;
     a.spin_ns = spin_ns_;
+    a.dbg = dbg_;
     a.trace = trace;
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)

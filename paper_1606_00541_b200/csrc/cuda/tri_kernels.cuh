@@ -44,6 +44,7 @@ struct WaveArgs {
     int ring_off;                // shared-memory byte offsets
     int buf_off;
     int buf_bytes;
+    int dbg;                     // experiment bits (HEC_WAVE_DBG; 0 in production)
     int spin_ns;                 // back-off inside the solvers' shared-memory spins (HEC_WAVE_SPIN_NS)
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
@@ -52,7 +53,7 @@ void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, c
 // kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise):
 // 16 solver warps with one row per lane, or one solver warp with rpl (2, 4, 8)
 // rows per lane
-void* wave_kernel(int width, int warps, int rpl, bool trace);
+void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;

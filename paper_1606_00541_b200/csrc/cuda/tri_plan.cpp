@@ -90,7 +90,6 @@ GridGeom detect_grid(const TriSource& s) {
 // 32 rows): the most CTAs that fit C, ties to square sub-tiles.
 bool pencil_owners(const GridGeom& g, int n, int C, int NW, std::vector<int>& owner, std::vector<int>& warp,
                    int& used) {
-    if (NW != 16) return false;
     int best = -1, bsx = 0, bsy = 0, bpx = 0, bpy = 0;
     for (int sx = 1; sx <= 32; ++sx)
         for (int sy = 1; sx * sy <= 32; ++sy) {
@@ -112,7 +111,7 @@ bool pencil_owners(const GridGeom& g, int n, int C, int NW, std::vector<int>& ow
         const int x = i % g.nx, y = (i / g.nx) % g.ny;
         const int px = x / tw, py = y / th;
         owner[i] = py * bpx + px;
-        warp[i] = ((y - py * th) / bsy) * 4 + (x - px * tw) / bsx;
+        warp[i] = (((y - py * th) / bsy) * 4 + (x - px * tw) / bsx) * NW / 16;  // 4x4 sub-tiles -> NW warps
     }
     used = bpx * bpy;
     return true;
@@ -197,8 +196,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     WaveLayout P;
     const int n = s.n;
     const int C0 = std::max(1, std::min(cfg.ctas, std::max(n, 1)));
-    int NW = std::max(1, std::min(cfg.warps, 32));
-    int warp_rows = cfg.warp_rows;
+    int NW = std::max(1, std::min(cfg.group > 0 ? cfg.group : 4, 16));  // warps per chunk (group size G)
+    int warp_rows = 32 * std::max(1, cfg.rpl);
     const int R = cfg.ring;
     P.n = n;
     P.nlev = s.nlev;
@@ -229,7 +228,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         return m;
     };
     bool use_pencils = false;
-    if (geo.ok && pencil_owners(geo, n, C0, NW, owner_i, warp_i, C_used)) {
+    if (geo.ok && pencil_owners(geo, n, C0, 16, owner_i, warp_i, C_used)) {
         const int per = (n + C0 - 1) / C0;
         std::vector<int> slab(n);
         for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
@@ -278,25 +277,33 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     P.ctas = C_used;
     const int C = C_used;
 
-    // one solver warp with two rows per lane when no CTA ever has more than 64
-    // rows in a level (e.g. 27-point slabs): no warp-to-warp synchronisation at all
-    P.rpl = 1;
-    if (cfg.auto_warps && !P.pencils && NW > 1 && n > 0) {
-        std::vector<int> lev_cnt(static_cast<std::size_t>(C), 0);
-        int worst = 0;
-        for (int k = 0; k < s.nlev && worst <= 64; ++k) {
-            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r)
-                worst = std::max(worst, ++lev_cnt[owner_i[s.inv_perm[r]]]);
-            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) lev_cnt[owner_i[s.inv_perm[r]]] = 0;
+    // solver shape: K groups of G warps take the chunks round robin, each chunk's
+    // rows dealt to its group's warps (RPL rows per lane). Auto: from the rows a
+    // CTA has in one level (95th percentile over the (CTA, level) pairs).
+    int K = std::max(1, cfg.groups);
+    if (cfg.group <= 0 && n > 0) {
+        std::vector<int> lev_cnt(static_cast<std::size_t>(C), 0), sizes;
+        for (int k = 0; k < s.nlev; ++k) {
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) ++lev_cnt[owner_i[s.inv_perm[r]]];
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) {
+                int& v = lev_cnt[owner_i[s.inv_perm[r]]];
+                if (v) sizes.push_back(v);
+                v = 0;
+            }
         }
-        if (worst <= 64) {
-            NW = 1;
-            P.rpl = 2;
-            warp_rows = 64;
-            std::fill(warp_i.begin(), warp_i.end(), 0);
-        }
+        auto p95 = sizes.begin() + static_cast<long>(sizes.size() * 95 / 100);
+        std::nth_element(sizes.begin(), p95, sizes.end());
+        const int m95 = sizes.empty() ? 0 : *p95;
+        if (m95 <= 64) { NW = 1; warp_rows = 64; K = 4; }
+        else if (m95 <= 128) { NW = 2; warp_rows = 64; K = 4; }
+        else { NW = 4; warp_rows = 128; K = 2; }
     }
-    P.warps = NW;
+    P.group = NW;
+    P.groups = K;
+    P.warps = NW * K;
+    P.rpl = std::max(1, warp_rows / 32);
+    P.lead = 1;  // chunks complete in order: no warp runs ahead of another
+    const bool lockstep = true;
 
     std::vector<int> cnt(n), owner_r(n), warp_r(n), nforeign(n, 0);
 #pragma omp parallel for schedule(static)
@@ -357,7 +364,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             for (int c = 0; c < C; ++c) {
                 auto& B = bucket[c];
                 if (B.empty()) continue;
-                std::stable_sort(B.begin(), B.end(), [&](int x, int y) { return warp_r[x] < warp_r[y]; });
+                if (!lockstep)
+                    std::stable_sort(B.begin(), B.end(), [&](int x, int y) { return warp_r[x] < warp_r[y]; });
                 std::size_t u = 0;
                 while (u < B.size()) {
                     Chunk ch{k, static_cast<int>(cta_rows[c].size()), 0, W, 0};
@@ -370,7 +378,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                         const int wcnt = warp_r[r] == cur_w ? cur_cnt + 1 : 1;
                         const int bytes =
                             wave_region_bytes(ch.m + 1, h2, wave_sections(ch.m + 1, W, NW, h2, t2, fl).end);
-                        if (ch.m > 0 && (wcnt > warp_rows || bytes > cfg.max_bytes)) break;
+                        const bool full = lockstep ? ch.m >= NW * warp_rows : wcnt > warp_rows;
+                        if (ch.m > 0 && (full || bytes > cfg.max_bytes)) break;
                         cur_w = warp_r[r];
                         cur_cnt = wcnt;
                         ch.ntail = t2;
@@ -378,6 +387,10 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                         cta_rows[c].push_back(r);
                         ++ch.m;
                         ++u;
+                    }
+                    if (lockstep) {  // deal the chunk's rows to the warps in contiguous segments
+                        const int pw = (ch.m + NW - 1) / NW;
+                        for (int t = 0; t < ch.m; ++t) warp_r[cta_rows[c][ch.row0 + t]] = t / pw;
                     }
                     per_cta[c].push_back(ch);
                 }

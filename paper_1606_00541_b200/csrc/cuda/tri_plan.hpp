@@ -107,9 +107,9 @@ LevelLayout build_levels(const TriSource& s);
 // from the blob start (b at -8*mb, staged halo at +bytes).
 struct WaveConfig {
     int ctas = 148;
-    int warps = 8;            // solver warps per CTA (<= 32)
-    int warp_rows = 32;       // max rows of one warp in one chunk (32 * rows per lane)
-    bool auto_warps = true;   // one solver warp (2 rows per lane) when every CTA level has <= 64 rows
+    int group = 0;            // solver warps per chunk (G); 0 = auto from the rows per (CTA, level)
+    int groups = 4;           // K groups of G warps take the chunks round robin
+    int rpl = 2;              // rows per lane (a warp takes up to 32 * rpl rows of a chunk)
     int ring = 8192;          // x ring entries (power of two); slot `ring` holds 0.0
     int inflight = 16;        // max chunks in flight per CTA (descriptor slots)
     int lead = 4;             // a warp starts chunk j only after every warp finished chunk j-lead
@@ -121,6 +121,7 @@ struct WaveConfig {
 
 struct WaveLayout {
     int n = 0, nlev = 0, ctas = 0, warps = 0, rpl = 1, ring = 0, inflight = 0, lead = 0;
+    int group = 1, groups = 1;            // solver shape: warps = group * groups
     int chunks = 0;
     int max_region = 0;                   // bytes of the largest chunk region
     int max_width = 0;                    // sliced-ELL width W of every chunk

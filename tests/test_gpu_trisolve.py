@@ -199,11 +199,15 @@ def test_wave_width_classes_and_splits(H, orc):
                 assert bits_equal(got, want), (w, upper)
 
 
-@pytest.mark.parametrize("knobs", [{}, {"HEC_WAVE_SLABS": "1"}, {"HEC_WAVE_RPL": "1"}, {"HEC_WAVE_RPL": "2"},
-                                   {"HEC_WAVE_RPL": "4"}, {"HEC_WAVE_RPL": "8"}])
+@pytest.mark.parametrize("knobs", [{}, {"HEC_WAVE_SLABS": "1"},
+                                   {"HEC_WAVE_G": "1", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_G": "1", "HEC_WAVE_K": "8", "HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_G": "4", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "4"},
+                                   {"HEC_WAVE_G": "4", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "4"}])
 def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
     # every row-ownership layout (z-pencils, slabs, strips) and solver shape
-    # (16 warps x 1 row, 1 warp x 2/4/8 rows) gives the reference's bits
+    # (G warps per chunk x K groups x RPL rows per lane) gives the reference's bits
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     rng = np.random.default_rng(23)
