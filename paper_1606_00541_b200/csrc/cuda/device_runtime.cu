@@ -79,6 +79,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
         if (const char* e = std::getenv("HEC_WAVE_DBG")) dbg_ = std::atoi(e);               // experiments only
         const int budget = smem_optin() - 1024;  // static shared + slack
+        cfg.smem_bytes = budget;
+        cfg.ctrl_bytes = kWaveCtrlBytes;
         plan::WaveLayout P;
         bool ok = true;
         try {
@@ -88,9 +90,10 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         }
         p_ring_ = cfg.ring;
         p_ring_off_ = kWaveCtrlBytes;
-        p_buf_off_ = rup(p_ring_off_ + 8 * (p_ring_ + 1), 128);
-        p_buf_bytes_ = (budget - p_buf_off_) / 16 * 16;
-        if (ok && 2 * P.max_region <= p_buf_bytes_) {
+        p_halo_ring_ = ok ? P.halo_ring : 32;
+        p_buf_off_ = ok ? P.buf_off : 0;
+        p_buf_bytes_ = ok ? P.buf_bytes : 0;
+        if (ok) {
             p_warps_ = P.warps;
             p_inflight_ = P.inflight;
             p_lead_ = P.lead;
@@ -234,6 +237,7 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
     a.inflight_log2 = __builtin_ctz(static_cast<unsigned>(p_inflight_));
     a.lead = p_lead_;
     a.ring = p_ring_;
+    a.halo_ring = p_halo_ring_;
     a.ring_off = p_ring_off_;
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;

@@ -41,6 +41,7 @@ struct WaveArgs {
     int inflight_log2;
     int lead;                    // max chunks a warp runs ahead of the slowest warp
     int ring;                    // x ring entries (power of two)
+    int halo_ring;               // H: staged-halo ring entries, behind the x ring
     int ring_off;                // shared-memory byte offsets
     int buf_off;
     int buf_bytes;
@@ -57,8 +58,9 @@ void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
+constexpr int kWaveProducers = 2;                      // producer warps (chunks round robin)
 constexpr int kWaveWaiters = 3;                        // waiter warps
-constexpr int kWaveRoleThreads = 32 * (1 + kWaveWaiters);  // producer warp + waiter warps
+constexpr int kWaveRoleThreads = 32 * (kWaveProducers + kWaveWaiters);
 constexpr int kWaveCtrlBytes = 1536;                   // control block at the start of shared memory
 
 }  // namespace hec::dev

@@ -426,6 +426,66 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     P.chunks = P.cta_chunk0[C];
 
+    // 2b. halo ring: the values a chunk reads from other CTAs are staged by the
+    //     waiters in a shared-memory ring of H entries behind the x ring, at
+    //     positions numbered per CTA in chunk order. A waiter stages chunk j only
+    //     after chunk j-NS finished (its descriptor slot was recycled), so H must
+    //     hold the halos of any NS consecutive chunks.
+    std::vector<std::vector<int>> hq0(C);
+    std::vector<int> hneed(C, 0);
+    {
+        std::vector<std::vector<int>> nh(C);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int c = 0; c < C; ++c) {
+            const auto& L = per_cta[c];
+            nh[c].resize(L.size());
+            std::vector<int> cols;
+            for (std::size_t j = 0; j < L.size(); ++j) {
+                cols.clear();
+                for (int t = 0; t < L[j].m; ++t) {
+                    const int r = cta_rows[c][L[j].row0 + t];
+                    if (nforeign[r])
+                        for_each_entry(s, r, [&](int col, double) {
+                            if (owner_r[col] != c) cols.push_back(col);
+                        });
+                }
+                std::sort(cols.begin(), cols.end());
+                nh[c][j] = static_cast<int>(std::unique(cols.begin(), cols.end()) - cols.begin());
+            }
+        }
+        auto need_for = [&](int ns) {
+            int worst = 0;
+            for (int c = 0; c < C; ++c) {
+                const auto& v = nh[c];
+                long long sum = 0;
+                for (std::size_t j = 0; j < v.size(); ++j) {
+                    sum += v[j];
+                    if (j >= static_cast<std::size_t>(ns)) sum -= v[j - ns];
+                    worst = static_cast<int>(std::max<long long>(worst, sum));
+                }
+            }
+            return worst;
+        };
+        int ns = P.inflight;
+        int need = need_for(ns);
+        while (need > cfg.halo_ring_max && ns > 2) need = need_for(ns /= 2);
+        if (need > cfg.halo_ring_max)
+            throw std::invalid_argument("hec_tri_create: halo ring overflow (wave layout)");
+        P.inflight = ns;
+        int H = 32;
+        while (H < need) H *= 2;
+        P.halo_ring = H;
+        for (int c = 0; c < C; ++c) {
+            hq0[c].resize(nh[c].size());
+            int q = 0;
+            for (std::size_t j = 0; j < nh[c].size(); ++j) {
+                hq0[c][j] = q & (H - 1);
+                q += nh[c][j];
+            }
+        }
+    }
+    const int H = P.halo_ring;
+
     // wave order: (CTA, chunk, row in chunk); bp[wave position] = b[bidx[..]]
     std::vector<long long> cta_wbase(static_cast<std::size_t>(C) + 1, 0);
     for (int c = 0; c < C; ++c) cta_wbase[c + 1] = cta_wbase[c] + static_cast<long long>(cta_rows[c].size());
@@ -474,7 +534,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             const int lo = qend[c][j] - win[c][j];
             halo_of.clear();
             halo.clear();
-            dep.assign(static_cast<std::size_t>(w) * mp, R);
+            dep.assign(static_cast<std::size_t>(w) * mp, 8 * R);  // padding: the 0.0 slot
             val.assign(static_cast<std::size_t>(w) * mp, 0.0);
             tptr.assign(round_up(mp + 1, 4), 0);
             tdep.clear();
@@ -496,7 +556,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                         if (chunk_pos_r[col] >= static_cast<int>(j)) seg_bad[c] = 1;
                         if (warp_r[col] != wr) mask[wr] |= 1u << warp_r[col];
                         if (seq_r[col] >= lo) {
-                            d = seq_r[col] & (R - 1);
+                            d = 8 * (seq_r[col] & (R - 1));
                             ++st_ring[c];
                         } else {
                             d = -(sol_index(s, col) + 1);
@@ -514,7 +574,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                         } else {
                             h = it->second;
                         }
-                        d = R + 1 + h;
+                        d = 8 * (R + 1 + ((hq0[c][j] + h) & (H - 1)));
                         ++st_halo[c];
                     }
                     if (e < w) {
@@ -541,7 +601,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             const std::size_t base = out.size();
             out.resize(base + round_up(sec.end, 16), 0);
             unsigned char* b = out.data() + base;
-            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, round_up(sec.end, 16)};
+            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, hq0[c][j]};
             std::memcpy(b, &hdr, sizeof(hdr));
             for (int wi = 0; wi < NW; ++wi) {
                 const unsigned a = t0[wi] < 0 ? 0u : (static_cast<unsigned>(t0[wi]) | (static_cast<unsigned>(t1[wi]) << 16));
@@ -582,6 +642,67 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     }
     for (int c = 0; c < C; ++c)
         if (seg_bad[c]) throw std::invalid_argument("hec_tri_create: dependency order violates the level schedule");
+
+    // 4b. shared-memory placement of every chunk's region, decided here so the
+    //     device producer only waits and copies. The regions form a byte ring of
+    //     buf_bytes; chunks are released in order (chunk j completes after j-1),
+    //     so a region may reuse the space of chunks up to `wait` once that chunk
+    //     is released; `wait` >= j - NS also recycles the descriptor slot.
+    {
+        const int x_end = cfg.ctrl_bytes + 8 * (R + 1 + P.halo_ring);
+        P.buf_off = round_up(x_end, 128);
+        P.buf_bytes = (cfg.smem_bytes - P.buf_off) / 16 * 16;
+        int rmax = 0;
+        for (int c = 0; c < C; ++c) rmax = std::max(rmax, region_max[c]);
+        if (cfg.smem_bytes > 0 && 2 * rmax > P.buf_bytes)
+            throw std::invalid_argument("hec_tri_create: chunk regions exceed shared memory (wave layout)");
+        const int B = P.buf_bytes, NS = P.inflight;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int c = 0; c < C; ++c) {
+            const int nc = static_cast<int>(per_cta[c].size());
+            std::vector<int> start(nc), end(nc);
+            int head = 0, oldest = 0;
+            for (int j = 0; j < nc; ++j) {
+                int* sp = &cta_span[c][8 * j];
+                const int need = sp[2];
+                int wait = j - NS;
+                oldest = std::max(oldest, j - NS + 1);
+                int pos;
+                for (;;) {
+                    if (oldest == j) {
+                        pos = 0;
+                        break;
+                    }
+                    const int tail = start[oldest];
+                    if (head >= tail) {
+                        if (head + need <= B) { pos = head; break; }
+                        if (need < tail) { pos = 0; break; }
+                    } else if (head + need < tail) {
+                        pos = head;
+                        break;
+                    }
+                    wait = std::max(wait, oldest);
+                    ++oldest;
+                }
+                start[j] = pos;
+                end[j] = pos + need;
+                head = pos + need;
+                // the producer warps take chunks round robin, so this chunk must itself
+                // wait for the newest older chunk whose space it reuses
+                for (int i = j - 1; i > wait; --i)
+                    if (pos < end[i] && start[i] < pos + need) {
+                        wait = i;
+                        break;
+                    }
+                sp[2] = pos;
+                sp[6] = wait;  // < 0: nothing to wait for
+                // invariant: disjoint from every chunk not yet known to be released
+                for (int i = std::max(0, wait + 1); i < j; ++i)
+                    if (pos < end[i] && start[i] < pos + need)
+                        throw std::logic_error("wave layout: region placement overlap");
+            }
+        }
+    }
 
     // 5. concatenate CTA streams
     std::size_t total = 0;

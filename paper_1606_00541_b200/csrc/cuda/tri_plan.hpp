@@ -115,6 +115,9 @@ struct WaveConfig {
     int lead = 4;             // a warp starts chunk j only after every warp finished chunk j-lead
     int max_bytes = 40960;    // chunk split: shared-memory region bytes
     int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
+    int halo_ring_max = 4096; // halo ring entries at most (shared memory)
+    int smem_bytes = 0;       // dynamic shared memory per CTA (0: skip the placement check)
+    int ctrl_bytes = 1536;    // control block in front of the x ring
     bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
     bool strips = true;       // row index follows the levels: every CTA takes a fraction of each level
 };
@@ -122,6 +125,8 @@ struct WaveConfig {
 struct WaveLayout {
     int n = 0, nlev = 0, ctas = 0, warps = 0, rpl = 1, ring = 0, inflight = 0, lead = 0;
     int group = 1, groups = 1;            // solver shape: warps = group * groups
+    int halo_ring = 32;                   // H: staged-halo ring entries (power of two)
+    int buf_off = 0, buf_bytes = 0;       // byte ring of chunk regions (shared-memory offsets)
     int chunks = 0;
     int max_region = 0;                   // bytes of the largest chunk region
     int max_width = 0;                    // sliced-ELL width W of every chunk
@@ -131,8 +136,9 @@ struct WaveLayout {
     bool strips = false;                  // every CTA owns a fraction of every level
     int grid_nx = 0, grid_ny = 0;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
-    std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region bytes, r0,
-                                          //              b area bytes, b copy bytes, 0, 0
+    std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region position in
+                                          //   the byte ring, r0, b area bytes, b copy bytes, chunk to wait
+                                          //   for (released before the region is reused; < 0: none), 0
     std::vector<int> bidx;                // n: input index of reordered row r (bp[r] = b[bidx[r]])
     std::vector<unsigned char> blob;      // all chunk blobs, 16-byte aligned
     long long ring_deps = 0, global_deps = 0, halo_deps = 0, halo_values = 0;
@@ -146,7 +152,7 @@ struct WaveSections {
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
     int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0
-    int nhalo, halo, tptr, bytes;  // halo id list / tail offsets, blob bytes (= staged halo offset)
+    int nhalo, halo, tptr, hq0;    // halo id list / tail offsets, halo ring position of the first staged value
 };
 static_assert(sizeof(WaveHeader) == 32, "wave header is two 16-byte words");
 constexpr int kWaveHeaderBytes = 32;
@@ -174,7 +180,8 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
 inline int wave_b_area(int m) { return 8 * round_up(m + 1, 4); }
 // shared-memory bytes of a chunk region: b + blob + staged halo
 inline int wave_region_bytes(int m, int nhalo, int blob_bytes) {
-    return wave_b_area(m) + round_up(blob_bytes, 16) + round_up(8 * nhalo, 16);
+    (void)nhalo;  // staged into the halo ring, not the region
+    return wave_b_area(m) + round_up(blob_bytes, 16);
 }
 
 }  // namespace hec::plan

@@ -1,7 +1,7 @@
-"""SM-cycle breakdown of one chunk for solver warp 5 (traced kernel, words 56..63),
-on the synthetic `chains` pattern of tools/wavebench.py (diagnostics).
+"""SM-clock stamps of solver warp 0 after its dependency wait (traced kernel,
+words 48..53) and the chunk period (diagnostics).
 
-python tools/stamps.py --S 64 512 --C 1
+python tools/stamps.py --stencil 7 --size 256      (or --chains S --C C)
 """
 import argparse
 import os
@@ -12,40 +12,51 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import paper_1606_00541_b200 as H  # noqa: E402
-from wavebench import build  # noqa: E402
 
-NAMES = ["bar_full", "header", "deps", "dd", "xv", "stored", "x", "published"]
+NAMES = ["(0)", "gathers", "fp", "stores", "arrive", "x stored"]
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--S", type=int, nargs="*", default=[64, 512])
-    ap.add_argument("--C", type=int, default=1)
+    ap.add_argument("--stencil", default="7")
+    ap.add_argument("--size", type=int, default=128)
+    ap.add_argument("--chains", type=int, default=0)
+    ap.add_argument("--C", type=int, default=148)
     ap.add_argument("--D", type=int, default=400)
-    ap.add_argument("--kind", default="chains")
     args = ap.parse_args()
     import torch
-    for S in args.S:
-        p = H.prepare_lower(build(args.kind, S, args.D, args.C))
-        t = H.DeviceTri.create(p, strategy=2, ctas=args.C)
-        b = torch.ones(p.n, dtype=torch.float64, device="cuda")
-        x = torch.empty_like(b)
-        for _ in range(2):
-            t.solve(b, x)
-        tr, c0 = t.solve_traced(b, x)
-        tr = tr.astype(np.int64)
-        nw = t.info()["threads"] // 32 - 4
-        ws = 5 if nw > 5 else 0  # the traced kernel stamps warp 5 (or warp 0)
-        cyc = tr[:, 56:64] if ws == 5 else tr[:, 48:56]
-        ok = cyc[:, 7] > 0
-        if not ok.any():
-            print(f"S={S}: no stamps (solver warp 5 absent: {t.info()['threads'] // 32 - 4} solver warps)")
-            continue
-        med = np.median(cyc[ok], axis=0)
-        done = tr[:, 10 + 3 * ws]
-        per = np.diff(done[c0[0]:c0[1]])
-        print(f"S={S} C={args.C} warps={nw}: chunk period p50 {np.median(per):.0f} ns; warp {ws} cycles from loop top: "
-              + "  ".join(f"{n} {int(v)}" for n, v in zip(NAMES, med)), flush=True)
+    if args.chains:
+        from wavebench import build
+        L = build("chains", args.chains, args.D, args.C)
+    else:
+        s = args.size
+        a = H.gen_poisson7(s, s, s) if args.stencil == "7" else H.gen_poisson27(s, s, s)
+        L = H.ilu0(a).l
+    p = H.prepare_lower(L)
+    t = H.DeviceTri.create(p, strategy=2, ctas=args.C)
+    b = torch.ones(p.n, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(b)
+    for _ in range(2):
+        t.solve(b, x)
+    tr, c0 = t.solve_traced(b, x)
+    tr = tr.astype(np.int64)
+    info = t.info()
+    cyc = tr[:, 48:54]
+    ok = cyc[:, 5] > 0
+    med = np.median(cyc[ok], axis=0)
+    T = np.where(tr > 0, tr - tr[:, 0].min(), -1)
+    nw = info["threads"] // 32 - 4
+    dd, dn = T[:, 9:9 + 3 * nw:3], T[:, 10:10 + 3 * nw:3]
+    last = dn.max(axis=1)
+    cm = (len(c0) - 1) // 2
+    per = np.diff(last[c0[cm]:c0[cm + 1]])
+    # handoff: chunk j released (deps) vs chunk j-1 done (max over its warps)
+    dmin = np.where(dd >= 0, dd, np.iinfo(np.int64).max).min(axis=1)
+    lo, hi = c0[cm], c0[cm + 1]
+    hand = dmin[lo + 1:hi] - last[lo:hi - 1]
+    print(f"{info['ctas']} CTAs x {nw} solver warps, chunks {info['chunks']}; CTA {cm}: period p50 {np.median(per):.0f} ns, "
+          f"release(j) - done(j-1) p50 {np.median(hand):.0f} ns; warp 0 cycles after its wait: "
+          + "  ".join(f"{n} {int(v)}" for n, v in zip(NAMES[1:], med[1:])), flush=True)
 
 
 if __name__ == "__main__":

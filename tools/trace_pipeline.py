@@ -61,15 +61,7 @@ def main():
     print("warp sees ready -> deps satisfied:   ", q((dd - rs)[busy]))
     print("deps satisfied -> warp done:         ", q((dn - dd)[busy]))
     print("first warp ready-seen -> last done:  ", q(last - rs.min(axis=1)))
-    names = ["bar_full ok", "header+seg", "deps ok", "row loads", "x deps loaded", "acc", "x", "published"]
-    for base, wname in ((48, "warp 0"), (56, "warp 5")):
-        cyc = tr[:, base:base + 8].astype(np.int64)
-        ok = cyc[:, 7] > 0
-        print(f"  {wname} SM cycles from loop top (p50): " +
-              "  ".join(f"{nm} {int(np.median(cyc[ok, k]))}" for k, nm in enumerate(names)))
-    for k, nm in enumerate(["drcp issued+diag", "accumulated", "divided", "stored"]):
-        v = tr[:, 56 + k]
-        print(f"   even-warp cycles to {nm:18s}", q(v[v > 0]))
+    # (SM-clock stamps of solver warp 0: tools/stamps.py)
     # per warp: how long after the previous chunk's done does it see ready
     for c in [0, 1, 70, len(c0) - 2]:
         lo, hi = c0[c], c0[c + 1]
