@@ -525,6 +525,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         auto& out = cta_blob[c];
         cta_span[c].assign(8 * L.size(), 0);
         std::unordered_map<int, int> halo_of;
+        struct HaloUse { int e, t, id; long long at; };  // at >= 0: ELL index, else -1 - tail index
+        std::vector<HaloUse> hpend;
         std::vector<int> halo, dep, tptr, tdep;
         std::vector<double> val, tval;
         for (std::size_t j = 0; j < L.size(); ++j) {
@@ -564,17 +566,10 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                             ++st_glob[c];
                         }
                     } else {
-                        const int id = export_id[col];
-                        auto it = halo_of.find(id);
-                        int h;
-                        if (it == halo_of.end()) {
-                            h = static_cast<int>(halo.size());
-                            halo_of.emplace(id, h);
-                            halo.push_back(id);
-                        } else {
-                            h = it->second;
-                        }
-                        d = 8 * (R + 1 + ((hq0[c][j] + h) & (H - 1)));
+                        // staged value: its halo-ring position is assigned below
+                        d = 0;
+                        hpend.push_back({e, t, export_id[col], e < w ? static_cast<long long>(e) * mp + t
+                                                                      : -1 - static_cast<long long>(tdep.size())});
                         ++st_halo[c];
                     }
                     if (e < w) {
@@ -589,6 +584,25 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 tptr[t + 1] = static_cast<int>(tdep.size());
             }
             for (int t = m; t < static_cast<int>(tptr.size()) - 1; ++t) tptr[t + 1] = tptr[t];
+            // halo-ring positions in (slot, row) order: the gather of ELL slot u by
+            // consecutive lanes then reads consecutive ring entries (no bank conflicts)
+            std::stable_sort(hpend.begin(), hpend.end(),
+                             [](const HaloUse& x, const HaloUse& y) { return x.e != y.e ? x.e < y.e : x.t < y.t; });
+            for (const HaloUse& hu : hpend) {
+                auto it = halo_of.find(hu.id);
+                int h;
+                if (it == halo_of.end()) {
+                    h = static_cast<int>(halo.size());
+                    halo_of.emplace(hu.id, h);
+                    halo.push_back(hu.id);
+                } else {
+                    h = it->second;
+                }
+                const int d = 8 * (R + 1 + ((hq0[c][j] + h) & (H - 1)));
+                if (hu.at >= 0) dep[static_cast<std::size_t>(hu.at)] = d;
+                else tdep[static_cast<std::size_t>(-1 - hu.at)] = d;
+            }
+            hpend.clear();
             const int nhalo = static_cast<int>(halo.size());
             const int ntail = static_cast<int>(tdep.size());
             st_hval[c] += nhalo;
