@@ -171,6 +171,7 @@ def run_ours(args, H, torch, rank, world, device):
     alg = alg_bytes(pl) + alg_bytes(pu)
     tl, tu, b, y, x, stream, ev, start, stop = time_device(H, torch, pl, pu, b_host, args.steps, args.warmup, device)
     info_l, info_u = tl.info(), tu.info()
+    log("[bench] warm-up done; timing")
     # our kernel launches per step: permute-in + persistent k_wave per triangle, or
     # one k_level_rows per level with the LEVELS strategy
     launches = sum(2 if i["strategy"] == 2 else i["nlev"] for i in (info_l, info_u))
@@ -224,6 +225,7 @@ def run_ours(args, H, torch, rank, world, device):
     u_res = float(np.max(np.abs(H.spmv_csr(f.u, xs, workers=os.cpu_count()) - ys)) /
                   max(1.0, float(np.max(np.abs(ys)))))
 
+    log(f"[bench] device step {ms_step:.3f} ms; end-to-end leg")
     # end to end through the C-ABI host entry, pinned buffers, copies inside the timed region
     dp = H.DevicePrecond.create(pl.n, pl, pu)
     bh = torch.empty(pl.n, dtype=torch.float64).pin_memory().numpy()
@@ -387,6 +389,7 @@ def secondary_device(H, torch, device, steps):
     stop.record(stream)
     torch.cuda.synchronize(device)
     ms = start.elapsed_time(stop) / steps
+    log(f"[bench] secondary {ms:.3f} ms per L+U step")
     peak, _ = measured_peak()
     gbs = alg / (ms * 1e-3) / 1e9
     return {"workload": cfg["workload"], "ms_per_step": round(ms, 4), "GB/s": round(gbs, 2),
@@ -403,6 +406,7 @@ def ras_gmres(H, torch, rank, world, device, size, restart=30):
     b = H.spmv_csr(a, np.ones(a.n_rows), workers=os.cpu_count())
     solver = ras.RasGmres(a, overlap=1, restart=restart, device=device)
     setup = time.time() - t0
+    log(f"[bench] RAS setup {setup:.1f}s; warm-up solve")
     solver.solve(b)  # warm-up: device layouts, workspaces, NCCL channels
     torch.cuda.synchronize(device)
     if world > 1:

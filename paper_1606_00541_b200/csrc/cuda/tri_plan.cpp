@@ -468,7 +468,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         };
         int ns = P.inflight;
         int need = need_for(ns);
-        while (need > cfg.halo_ring_max && ns > 2) need = need_for(ns /= 2);
+        while (need > cfg.halo_ring_max && ns > 4) need = need_for(ns /= 2);  // NS >= 4 (kernel slot waits)
         if (need > cfg.halo_ring_max)
             throw std::invalid_argument("hec_tri_create: halo ring overflow (wave layout)");
         P.inflight = ns;
