@@ -257,3 +257,22 @@ def test_cuda_graph_replay(H, orc):
         g.replay()
         torch.cuda.synchronize()
         assert bits_equal(x.cpu().numpy(), orc.solve(ou, orc.solve(ol, b))), rep
+
+
+def test_signed_zero_rhs(H, orc):
+    # b = A * 1 leaves exact zeros in the interior (the bench right-hand side);
+    # zero numerators take the kernel's a * RN(1/d) shortcut and must keep the
+    # IEEE sign of 0 / d, bitwise
+    for gen, dims in (("gen_poisson27", (14, 13, 12)), ("gen_poisson7", (22, 21, 20))):
+        a = getattr(H, gen)(*dims)
+        f = H.ilu0(a)
+        b = H.spmv_csr(a, np.ones(a.n_rows))
+        rng = np.random.default_rng(31)
+        neg = rng.random(a.n_rows) < 0.3
+        b[(b == 0) & neg] = -0.0
+        for fac, upper in ((f.l, False), (f.u, True)):
+            p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+            want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+            got, _ = device_solve(H, p, b, 2)
+            assert bits_equal(got, want), (gen, upper)
+            assert (np.signbit(got) == np.signbit(want)).all()

@@ -57,6 +57,20 @@ int main(int argc, char** argv) {
             ++bad;
         }
     }
-    printf("samples %lld mismatches %lld guarded(slow path) %lld\n", n, bad, guarded);
+    /* zero numerators: the kernel returns RN(a * y) when y is finite and nonzero */
+    long long zeros = 0;
+    for (long long i = 0; i < n / 100; ++i) {
+        const double d = mk(mant_sample(), (int)(next() % 2047) - 1023, next() & 1);
+        const double a = (next() & 1) ? -0.0 : 0.0;
+        const double y = 1.0 / d;
+        if (!(fabs(y) > 0.0 && fabs(y) < INFINITY)) continue;
+        const double q = a * y, want = a / d;
+        ++zeros;
+        if (memcmp(&q, &want, 8) != 0) {
+            if (bad < 10) printf("ZERO MISMATCH a=%a d=%a got %a want %a\n", a, d, q, want);
+            ++bad;
+        }
+    }
+    printf("samples %lld mismatches %lld guarded(slow path) %lld zero-numerator samples %lld\n", n, bad, guarded, zeros);
     return bad != 0;
 }
