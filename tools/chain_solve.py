@@ -20,9 +20,10 @@ def main():
     ap.add_argument("--D", type=int, default=2000)
     ap.add_argument("--kind", default="chains")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--extra", type=int, default=0)
     args = ap.parse_args()
     import torch
-    p = H.prepare_lower(build(args.kind, args.S, args.D, args.C))
+    p = H.prepare_lower(build(args.kind, args.S, args.D, args.C, args.extra))
     t = H.DeviceTri.create(p, strategy=2, ctas=args.C)
     b = torch.ones(p.n, dtype=torch.float64, device="cuda")
     x = torch.empty_like(b)

@@ -21,7 +21,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1606_00541_b200 as H  # noqa: E402
 
 
-def build(kind, S, D, C):
+def build(kind, S, D, C, extra=0):
     # index of (block, s, k) = block*S*D + s*D + k  (column-major chains)
     rows, cols, vals = [], [], []
     nb = C if kind in ("chains", "warps") else 1
@@ -32,6 +32,9 @@ def build(kind, S, D, C):
     rows.append(idx.ravel()); cols.append(idx.ravel()); vals.append(np.full(n, 4.0))
     # (s,k) <- (s,k-1)
     rows.append(idx[:, :, 1:].ravel()); cols.append(idx[:, :, :-1].ravel()); vals.append(np.full(nb * SS * (D - 1), -1.0))
+    for e in range(1, min(extra, SS - 1) + 1):  # wider rows: (s, k) <- (s - e, k - 1)
+        dst, src = idx[:, e:, 1:], idx[:, :-e, :-1]
+        rows.append(dst.ravel()); cols.append(src.ravel()); vals.append(np.full(dst.size, -0.01))
     if kind in ("warps", "ctas"):
         rows.append(idx[:, 1:, 1:].ravel()); cols.append(idx[:, :-1, :-1].ravel())
         vals.append(np.full(nb * (SS - 1) * (D - 1), -0.5))
@@ -53,11 +56,12 @@ def main():
     ap.add_argument("--kinds", nargs="*", default=["chains", "warps", "ctas"])
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--extra", type=int, default=0, help="extra dependencies per row (row width 1 + extra)")
     args = ap.parse_args()
     import torch
     for kind in args.kinds:
         t0 = time.time()
-        L = build(kind, args.S, args.D, args.C)
+        L = build(kind, args.S, args.D, args.C, args.extra)
         p = H.prepare_lower(L)
         t = H.DeviceTri.create(p, strategy=2, ctas=args.C, threads=args.threads)
         info = t.info()
