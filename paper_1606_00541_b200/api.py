@@ -397,6 +397,16 @@ class DeviceTri:
         check(lib.hec_tri_solve_ordered(self._h, C.c_void_p(_ptr(bp_dev)), C.c_void_p(_ptr(x_dev)),
                                         C.c_void_p(_stream(stream)) if stream is not None else None))
 
+    def solve_wave(self, bp_dev, xw_dev, stream=None) -> None:
+        """The solve alone, x left in the layout's wave order (see permute_out)."""
+        check(lib.hec_tri_solve_wave(self._h, C.c_void_p(_ptr(bp_dev)), C.c_void_p(_ptr(xw_dev)),
+                                     C.c_void_p(_stream(stream)) if stream is not None else None))
+
+    def permute_out(self, xw_dev, x_dev, stream=None) -> None:
+        """x[o] = xw[wpos[o]]: the solution order from solve_wave's output."""
+        check(lib.hec_tri_permute_out(self._h, C.c_void_p(_ptr(xw_dev)), C.c_void_p(_ptr(x_dev)),
+                                      C.c_void_p(_stream(stream)) if stream is not None else None))
+
     def solve_host(self, b) -> np.ndarray:
         bv = _f64_vec(b, None, "solve")
         x = np.empty_like(bv)

@@ -336,6 +336,26 @@ int hec_tri_solve_ordered(hec_tri_t t, const double* bp_dev, double* x_dev, void
     });
 }
 
+int hec_tri_solve_wave(hec_tri_t t, const double* bp_dev, double* xw_dev, void* stream) {
+    return guarded([&] {
+        need(t, "hec_tri_solve_wave");
+        if (t->impl->n() > 0 && (!bp_dev || !xw_dev)) throw std::invalid_argument("hec_tri_solve_wave: null vector");
+        if (bp_dev == xw_dev && t->impl->n() > 0)
+            throw std::invalid_argument("hec_tri_solve_wave: bp and xw must not alias");
+        t->impl->solve_wave(bp_dev, xw_dev, nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int hec_tri_permute_out(hec_tri_t t, const double* xw_dev, double* x_dev, void* stream) {
+    return guarded([&] {
+        need(t, "hec_tri_permute_out");
+        if (t->impl->n() > 0 && (!xw_dev || !x_dev)) throw std::invalid_argument("hec_tri_permute_out: null vector");
+        if (xw_dev == x_dev && t->impl->n() > 0)
+            throw std::invalid_argument("hec_tri_permute_out: xw and x must not alias");
+        t->impl->permute_out(xw_dev, x_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int hec_tri_solve_traced(hec_tri_t t, const double* b_dev, double* x_dev, void* stream,
                          unsigned long long* trace_dev, int* cta_chunk0) {
     return guarded([&] {

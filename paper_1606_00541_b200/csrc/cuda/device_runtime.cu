@@ -117,6 +117,9 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_bidx_.upload(P.bidx);
             p_cta0_.upload(P.cta_chunk0);
             p_cta0_host_ = P.cta_chunk0;
+            p_wpos_.upload(P.wpos);
+            h_wpos_ = P.wpos;
+            h_bidx_ = P.bidx;
             stats_.ctas = p_ctas_;
             stats_.threads = kWaveRoleThreads + 32 * p_warps_;
             if (!p_kernel_) throw std::invalid_argument("hec_tri_create: no wave kernel for this width");
@@ -134,6 +137,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         l_width_ = L.width;
         l_ld_ = L.ld;
         l_bidx_.upload(L.bidx);
+        h_bidx_ = L.bidx;
+        h_wpos_.clear();  // level launches write x in solution order
         l_xidx_.upload(L.xidx);
         if (has_out_) l_oidx_.upload(L.oidx);
         l_ell_dep_.upload(L.ell_dep);
@@ -157,7 +162,7 @@ DeviceTri::~DeviceTri() {
 
 int DeviceTri::launches_per_solve() const {
     if (n_ == 0) return 0;
-    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 2;  // permute-in + wave
+    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 3;  // permute-in + wave + permute-out
 }
 
 DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
@@ -170,6 +175,7 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
         HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
         w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
         w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
+        w->xw.alloc(static_cast<std::size_t>(std::max(n_, 1)));
         HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
         HEC_CUDA(cudaDeviceSynchronize());
     }
@@ -191,6 +197,15 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st,
     Workspace& w = workspace(st);
     permute(b, w.bp.p, st);
     solve_ordered(w.bp.p, xs, out, st, trace);
+}
+void DeviceTri::permute_out(const double* xw, double* xs, cudaStream_t st) const {
+    if (n_ == 0 || !xs) return;
+    if (strategy_ == 1) {  // level launches already write the solution order
+        if (xw != xs) HEC_CUDA(cudaMemcpyAsync(xs, xw, sizeof(double) * n_, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    permute_in(xw, p_wpos_.p, xs, n_, st);  // xs[o] = xw[wpos[o]]: coalesced writes
+    HEC_CUDA(cudaGetLastError());
 }
 
 void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st) {
@@ -223,12 +238,22 @@ void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStr
         return;
     }
     Workspace& w = workspace(st);
+    solve_wave(bp, w.xw.p, out, st, trace);
+    permute_out(w.xw.p, xs, st);
+}
+void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream_t st, unsigned long long* trace) {
+    if (n_ == 0) return;
+    if (strategy_ == 1) {
+        run_levels(bp, true, xw, out, st);
+        return;
+    }
+    Workspace& w = workspace(st);
     WaveArgs a{};
     a.blobs = p_blob_.p;
     a.spans = reinterpret_cast<const int4*>(p_spans_.p);
     a.cta_chunk0 = p_cta0_.p;
     a.bp = bp;
-    a.xs = xs;
+    a.xs = xw;
     a.out = has_out_ ? out : nullptr;
     a.mbox = w.mailbox.p;
     a.counters = w.counters.p;
@@ -286,6 +311,7 @@ DevicePrecond::DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, 
     u.out_map = out_index;
     l_ = std::make_unique<DeviceTri>(l, opt);
     u_ = std::make_unique<DeviceTri>(u, opt);
+    compose();
 }
 
 DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
@@ -312,6 +338,7 @@ DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* ow
     }
     l_ = std::make_unique<DeviceTri>(l, opt);
     u_ = std::make_unique<DeviceTri>(u, opt);
+    compose();
 }
 
 DevicePrecond::~DevicePrecond() {
@@ -323,8 +350,10 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
     auto& w = ws_[st];
     if (!w) {
         w = std::make_unique<Workspace>();
-        w->y.alloc(std::max(n_ext_, 1));
-        if (!identity_) w->z.alloc(std::max(n_ext_, 1));
+        w->bl.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
+        w->yw.alloc(std::max(n_ext_, 1));
+        w->bu.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
+        w->xw.alloc(std::max(n_ext_, 1));
     }
     return *w;
 }
@@ -332,11 +361,26 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
 void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
     if (n_ext_ == 0) return;
     Workspace& w = workspace(st);
-    l_->solve(r, w.y.p, nullptr, st);
-    if (identity_)
-        u_->solve(w.y.p, x, nullptr, st);
-    else
-        u_->solve(w.y.p, w.z.p, x, st);
+    // L from r gathered into its row order, its output left in wave order; U's
+    // right-hand side is gathered straight from there through the composed map
+    // (no pass through the solution order in between)
+    l_->permute(r, w.bl.p, st);
+    l_->solve_wave(w.bl.p, w.yw.p, nullptr, st);
+    permute_in(w.yw.p, lu_map_.p, w.bu.p, n_ext_, st);
+    HEC_CUDA(cudaGetLastError());
+    if (identity_) {
+        u_->solve_wave(w.bu.p, w.xw.p, nullptr, st);
+        u_->permute_out(w.xw.p, x, st);
+    } else {
+        u_->solve_wave(w.bu.p, w.xw.p, x, st);  // owned rows scattered into x by the kernel
+    }
+}
+void DevicePrecond::compose() {
+    const std::vector<int>& bu = u_->host_bidx();
+    const std::vector<int>& wl = l_->host_wpos();
+    std::vector<int> m(static_cast<std::size_t>(n_ext_));
+    for (int p = 0; p < n_ext_; ++p) m[p] = wl.empty() ? bu[p] : wl[bu[p]];
+    lu_map_.upload(m);
 }
 
 void DevicePrecond::apply_host(const double* r, double* x) {

@@ -85,6 +85,15 @@ public:
     void permute(const double* b, double* bp, cudaStream_t st) const;
     void solve_ordered(const double* bp, double* xs, double* out, cudaStream_t st,
                        unsigned long long* trace = nullptr);
+    // The solve alone: x in *wave order* (xw[wave position]; the solution order for
+    // the level strategy), then permute_out gives xs[o] = xw[wpos[o]].
+    void solve_wave(const double* bp, double* xw, double* out, cudaStream_t st,
+                    unsigned long long* trace = nullptr);
+    void permute_out(const double* xw, double* xs, cudaStream_t st) const;
+    // host copies of the maps: bidx (reordered input) and wpos (solution index ->
+    // output position; empty = identity)
+    const std::vector<int>& host_bidx() const { return h_bidx_; }
+    const std::vector<int>& host_wpos() const { return h_wpos_; }
     // chunk -> CTA map of the pipeline layout (empty for LEVELS)
     const std::vector<int>& cta_chunk0() const { return p_cta0_host_; }
     // Synchronous host-vector convenience (pinned or pageable).
@@ -98,6 +107,7 @@ private:
         DevBuf<uint32_t> counters;            // ticket, finished CTAs, mailbox epoch
         DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
         DevBuf<double> bp;                    // right-hand side in reordered-row order
+        DevBuf<double> xw;                    // solution in wave order
     };
     Workspace& workspace(cudaStream_t st);
     void run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st);
@@ -113,7 +123,8 @@ private:
     bool has_out_ = false;
     // WAVE (persistent wavefront kernel)
     DevBuf<unsigned char> p_blob_;
-    DevBuf<int> p_spans_, p_cta0_, p_bidx_;
+    DevBuf<int> p_spans_, p_cta0_, p_bidx_, p_wpos_;
+    std::vector<int> h_bidx_, h_wpos_;
     int p_ctas_ = 0, p_inflight_ = 0, p_ring_ = 0, p_ring_off_ = 0, p_buf_off_ = 0, p_buf_bytes_ = 0;
     int p_smem_ = 0, p_warps_ = 0, p_lead_ = 1, spin_ns_ = 0, p_rpl_ = 1, dbg_ = 0, p_halo_ring_ = 32;
     void* p_kernel_ = nullptr;
@@ -148,11 +159,13 @@ public:
 
 private:
     struct Workspace {
-        DevBuf<double> y, z;
+        DevBuf<double> bl, yw, bu, xw;  // L input (reordered), L output (wave), U input, U output
     };
     int n_ = 0, n_out_ = 0, n_ext_ = 0;
     bool identity_ = true;
     std::unique_ptr<DeviceTri> l_, u_;
+    DevBuf<int> lu_map_;  // U input position -> L output position (the two permutations composed)
+    void compose();
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
     std::mutex h_mu_;

@@ -490,11 +490,19 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     std::vector<long long> cta_wbase(static_cast<std::size_t>(C) + 1, 0);
     for (int c = 0; c < C; ++c) cta_wbase[c + 1] = cta_wbase[c] + static_cast<long long>(cta_rows[c].size());
     P.bidx.assign(n, 0);
+    P.wpos.assign(n, 0);
+    std::vector<int> wpos_r(n);  // reordered row -> wave position
 #pragma omp parallel for schedule(static)
     for (int r = 0; r < n; ++r) {
         const int o = sol_index(s, r);
-        P.bidx[cta_wbase[owner_r[r]] + seq_r[r]] = s.b_map ? s.b_map[o] : o;
+        const int p = static_cast<int>(cta_wbase[owner_r[r]] + seq_r[r]);
+        wpos_r[r] = p;
+        P.bidx[p] = s.b_map ? s.b_map[o] : o;
+        P.wpos[o] = p;
     }
+    // x is written in wave order (coalesced stores; the solution order is one
+    // gather pass away) unless cfg.wave_x is off
+    auto x_index = [&](int r) { return cfg.wave_x ? wpos_r[r] : sol_index(s, r); };
 
     // 3. exports: rows read by another CTA get a mailbox id
     std::vector<int> export_id(n, -1);
@@ -561,7 +569,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                             d = 8 * (seq_r[col] & (R - 1));
                             ++st_ring[c];
                         } else {
-                            d = -(sol_index(s, col) + 1);
+                            d = -(x_index(col) + 1);
                             glob = true;
                             ++st_glob[c];
                         }
@@ -629,7 +637,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 const int r = cta_rows[c][ch.row0 + t];
                 const int o = sol_index(s, r);
                 put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
-                put_i(sec.xidx, t, o);
+                put_i(sec.xidx, t, x_index(r));
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
                 put_i(sec.exp, t, export_id[r]);
             }

@@ -116,6 +116,7 @@ struct WaveConfig {
     int max_bytes = 40960;    // chunk split: shared-memory region bytes
     int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
     int halo_ring_max = 4096; // halo ring entries at most (shared memory)
+    bool wave_x = true;       // x written in wave order (else scattered to the solution index)
     int smem_bytes = 0;       // dynamic shared memory per CTA (0: skip the placement check)
     int ctrl_bytes = 1536;    // control block in front of the x ring
     bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
@@ -136,6 +137,7 @@ struct WaveLayout {
     bool strips = false;                  // every CTA owns a fraction of every level
     int grid_nx = 0, grid_ny = 0;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
+    std::vector<int> wpos;                // solution index -> wave position (where x lands)
     std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region position in
                                           //   the byte ring, r0, b area bytes, b copy bytes, chunk to wait
                                           //   for (released before the region is reused; < 0: none), 0

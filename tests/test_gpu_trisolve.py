@@ -276,3 +276,28 @@ def test_signed_zero_rhs(H, orc):
             got, _ = device_solve(H, p, b, 2)
             assert bits_equal(got, want), (gen, upper)
             assert (np.signbit(got) == np.signbit(want)).all()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_wave_order_output(H, orc, strategy):
+    # hec_tri_solve_wave leaves x in wave order; hec_tri_permute_out restores the
+    # solution order bitwise; the wave output is a permutation of the solution
+    torch = pytest.importorskip("torch")
+    a = H.gen_poisson7(19, 18, 17)
+    f = H.ilu0(a)
+    rng = np.random.default_rng(37)
+    for fac, upper in ((f.l, False), (f.u, True)):
+        p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+        t = H.DeviceTri.create(p, strategy=strategy)
+        b = rng.uniform(-1, 1, a.n_rows)
+        want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+        bd = torch.tensor(b, device="cuda")
+        bp = torch.empty(a.n_rows + 2, dtype=torch.float64, device="cuda")
+        xw = torch.empty_like(bd)
+        x = torch.full_like(bd, float("nan"))
+        t.permute_in(bd, bp)
+        t.solve_wave(bp, xw)
+        t.permute_out(xw, x)
+        torch.cuda.synchronize()
+        assert bits_equal(x.cpu().numpy(), want)
+        assert np.array_equal(np.sort(xw.cpu().numpy().view(np.uint64)), np.sort(want.view(np.uint64)))
