@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--C", type=int, default=1)
     ap.add_argument("--D", type=int, default=2000)
     ap.add_argument("--cta", type=int, default=-1)
+    ap.add_argument("--extra", type=int, default=0)
     ap.add_argument("--first", type=int, default=200)
     ap.add_argument("--count", type=int, default=12)
     args = ap.parse_args()
@@ -32,7 +33,7 @@ def main():
         L = H.ilu0(a).l
     else:
         from wavebench import build
-        L = build("chains", args.chains, args.D, args.C)
+        L = build("chains", args.chains, args.D, args.C, args.extra)
     p = H.prepare_lower(L)
     t = H.DeviceTri.create(p, strategy=2, ctas=args.C if not args.size else 0)
     b = torch.ones(p.n, dtype=torch.float64, device="cuda")
