@@ -77,7 +77,6 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         }
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
-        if (const char* e = std::getenv("HEC_WAVE_DBG")) dbg_ = std::atoi(e);               // experiments only
         const int budget = smem_optin() - 1024;  // static shared + slack
         cfg.smem_bytes = budget;
         cfg.ctrl_bytes = kWaveCtrlBytes;
@@ -267,7 +266,6 @@ void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;
     a.spin_ns = spin_ns_;
-    a.dbg = dbg_;
     a.trace = trace;
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)

@@ -45,7 +45,6 @@ struct WaveArgs {
     int ring_off;                // shared-memory byte offsets
     int buf_off;
     int buf_bytes;
-    int dbg;                     // experiment bits (HEC_WAVE_DBG; 0 in production)
     int spin_ns;                 // back-off inside the solvers' shared-memory spins (HEC_WAVE_SPIN_NS)
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };

@@ -33,6 +33,11 @@
 namespace hec::dev {
 
 // -------------------------------------------------------------- LEVELS ----
+// IEEE row update, never contracted into an FMA.
+__device__ __forceinline__ double sub_prod(double acc, double v, double x) {
+    return __dsub_rn(acc, __dmul_rn(v, x));
+}
+
 __global__ void k_level_rows(LevelArgs a, int r0, int r1) {
     const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= r1) return;
