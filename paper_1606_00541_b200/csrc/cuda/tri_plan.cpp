@@ -501,8 +501,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         P.wpos[o] = p;
     }
     // x is written in wave order (coalesced stores; the solution order is one
-    // gather pass away) unless cfg.wave_x is off
-    auto x_index = [&](int r) { return cfg.wave_x ? wpos_r[r] : sol_index(s, r); };
+    // gather pass away): a row older than the ring window is re-read there
+    auto x_index = [&](int r) { return wpos_r[r]; };
 
     // 3. exports: rows read by another CTA get a mailbox id
     std::vector<int> export_id(n, -1);
@@ -623,7 +623,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             const std::size_t base = out.size();
             out.resize(base + round_up(sec.end, 16), 0);
             unsigned char* b = out.data() + base;
-            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, hq0[c][j]};
+            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, hq0[c][j], static_cast<int>(wpos), 0, 0, 0};
             std::memcpy(b, &hdr, sizeof(hdr));
             for (int wi = 0; wi < NW; ++wi) {
                 const unsigned a = t0[wi] < 0 ? 0u : (static_cast<unsigned>(t0[wi]) | (static_cast<unsigned>(t1[wi]) << 16));
@@ -637,7 +637,6 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 const int r = cta_rows[c][ch.row0 + t];
                 const int o = sol_index(s, r);
                 put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
-                put_i(sec.xidx, t, x_index(r));
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
                 put_i(sec.exp, t, export_id[r]);
             }

@@ -95,7 +95,8 @@ LevelLayout build_levels(const TriSource& s);
 //   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep R)
 //   int    dep[W][mp]    0 <= d < R: ring slot; d == R: 0.0 (padding);
 //                        d > R: staged halo value d-R-1; d < 0: x[-d-1]
-//   int xidx[mp], exp[mp] (mailbox id or -1), (oidx[mp] if flags&2)
+//   int exp[mp] (mailbox id or -1), (oidx[mp] if flags&2); row t's x goes to
+//   wave position r0 + t (header), so no per-row solution index is stored
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
 //   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages
 // The right-hand side arrives permuted into reordered-row order (bp[r] =
@@ -116,7 +117,6 @@ struct WaveConfig {
     int max_bytes = 40960;    // chunk split: shared-memory region bytes
     int max_width = 16;       // sliced-ELL width cap; longer rows spill to the tail
     int halo_ring_max = 4096; // halo ring entries at most (shared memory)
-    bool wave_x = true;       // x written in wave order (else scattered to the solution index)
     int smem_bytes = 0;       // dynamic shared memory per CTA (0: skip the placement check)
     int ctrl_bytes = 1536;    // control block in front of the x ring
     bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
@@ -148,16 +148,17 @@ struct WaveLayout {
 WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg);
 
 struct WaveSections {
-    int seg, diag, val, dep, xidx, exp, oidx, tptr, tval, tdep, halo, end;
+    int seg, diag, val, dep, exp, oidx, tptr, tval, tdep, halo, end;
 };
 
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
     int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0
     int nhalo, halo, tptr, hq0;    // halo id list / tail offsets, halo ring position of the first staged value
+    int r0, pad0, pad1, pad2;      // wave position of the chunk's first row (where its x values go)
 };
-static_assert(sizeof(WaveHeader) == 32, "wave header is two 16-byte words");
-constexpr int kWaveHeaderBytes = 32;
+static_assert(sizeof(WaveHeader) == 48, "wave header is three 16-byte words");
+constexpr int kWaveHeaderBytes = 48;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 // Offsets of the fixed sections (also computed this way on the device).
@@ -169,7 +170,6 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     b.diag = at;  at += 8 * mp;
     b.val = at;   at += 8 * mp * w;
     b.dep = at;   at += 4 * mp * w;
-    b.xidx = at;  at += 4 * mp;
     b.exp = at;   at += 4 * mp;
     b.oidx = at;  if (flags & 2) at += 4 * mp;
     b.tptr = at;  if (flags & 1) at += 4 * round_up(mp + 1, 4);
