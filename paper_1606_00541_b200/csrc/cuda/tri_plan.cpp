@@ -281,6 +281,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     // rows dealt to its group's warps (RPL rows per lane). Auto: from the rows a
     // CTA has in one level (95th percentile over the (CTA, level) pairs).
     int K = std::max(1, cfg.groups);
+    bool big_auto = false;  // > 128 rows per CTA level: 4x2x4, or 8x2x2 for narrow rows (below)
     if (cfg.group <= 0 && n > 0) {
         std::vector<int> lev_cnt(static_cast<std::size_t>(C), 0), sizes;
         for (int k = 0; k < s.nlev; ++k) {
@@ -296,7 +297,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         const int m95 = sizes.empty() ? 0 : *p95;
         if (m95 <= 64) { NW = 1; warp_rows = 64; K = 4; }
         else if (m95 <= 128) { NW = 2; warp_rows = 64; K = 4; }
-        else { NW = 4; warp_rows = 128; K = 2; }
+        else { NW = 4; warp_rows = 128; K = 2; big_auto = true; }
     }
     P.group = NW;
     P.groups = K;
@@ -349,6 +350,15 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         }
     }
     const int W = P.max_width;
+    if (big_auto && W <= 4) {  // narrow rows: 8 warps x 2 rows per lane fit 96 registers (measured ~1.5 % faster)
+        NW = 8;
+        warp_rows = 64;
+        K = 2;
+        P.group = NW;
+        P.groups = K;
+        P.warps = NW * K;
+        P.rpl = 2;
+    }
 
     // 1. chunk discovery: per level, each CTA's rows (ordered by warp, then by
     //    row, so every warp's rows are one segment), split so that no warp has
