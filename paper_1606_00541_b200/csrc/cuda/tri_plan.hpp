@@ -55,57 +55,53 @@ LevelLayout build_levels(const TriSource& s);
 // ------------------------------------------------------------------ WAVE ----
 // Persistent wavefront kernel (one CTA per SM, cooperative launch so every
 // CTA is resident). Row ownership, in the lower frame:
-//  * default: CTA c owns rows [c*per, (c+1)*per) ("slabs"), solver warp w a
-//    contiguous sub-range of those;
+//  * default: CTA c owns rows [c*per, (c+1)*per) ("slabs");
 //  * when the row index follows the levels (an RCM-like ordering), slabs would
 //    hand each CTA a few consecutive levels only: then "strips" -- each CTA
 //    owns the c-th fraction of every level;
 //  * when the factor is recognised as a structured nx x ny x nz grid in natural
 //    order (its dependency offsets are {1, nx, nx*ny} or the 27-point set),
-//    CTA (px, py) owns the z-pencil of an x-y tile and warp w a 2-D sub-tile of
-//    it. A wavefront then crosses ~sqrt(C) CTA boundaries per direction instead
-//    of C, and every level keeps all warps of an active CTA busy.
-// The CTA's rows of one level form a "chunk" (ordered by warp, then by row, and
-// split so that no warp has more than 32 rows); rows are numbered in "wave
-// order" (CTA, chunk, row) and the right-hand side is permuted into that order.
+//    CTA (px, py) owns the z-pencil of an x-y tile. A wavefront then crosses
+//    ~sqrt(C) CTA boundaries per direction instead of C.
+// The CTA's rows of one level form a "chunk" (split at the solver shape's
+// capacity G x 32 x RPL rows and at max_bytes of shared memory); rows are
+// numbered in "wave order" (CTA, chunk, row), the right-hand side is permuted
+// into that order and x is written in it.
 //
 // Synchronisation replaces the reference's per-level barrier
 // (triangular.cpp:128) by dataflow:
-//   * inside a CTA: per-warp progress counters in shared memory; a warp
-//     starts its segment of chunk j once every warp it reads from (the
-//     segment's source mask) has finished chunk j-1;
+//   * inside a CTA: K groups of G solver warps take the chunks round robin; a
+//     named barrier orders chunk j after chunk j-1, so chunks complete in order
+//     (lead = 1: an own row is safe in the x ring while it is newer than
+//     q_end(j) - R);
 //   * across CTAs: rows read by another CTA are "exported": the producing
 //     thread writes the value into a 16-byte mailbox as two 8-byte words
 //     {lo32 | epoch, hi32 | epoch}; the consumer's waiter warps poll until
-//     both words carry the current solve's epoch, then stage the value in
-//     shared memory. Epochs advance per solve, so mailboxes are never reset.
-// Own-CTA values come from a shared-memory ring indexed by the CTA's row
-// sequence number; values older than the ring window are re-read from x.
-// No warp runs more than `lead`-1 chunks ahead of the slowest one, so an entry
-// read in chunk j is safe in the ring while it is newer than
-// q_end(j) - (R - rows of chunks j+1 .. j+lead-1).
+//     both words carry the current solve's epoch, then stage the value in the
+//     shared-memory halo ring. Epochs advance per solve, so mailboxes are
+//     never reset.
 //
 // Blob of one chunk (16-byte aligned, moved by one cp.async.bulk); mp =
-// round_up(m, 4), W = the layout's sliced-ELL width, NW = solver warps. Every
-// section before the tail sits at an offset computable from mp alone, so the
-// kernel reads only the 32-byte header and its warp's descriptor:
-//   WaveHeader (32 B)  {m, mp, q0, flags}, {nhalo, halo list, tail, bytes}
-//   uint2 seg[NW]        per solver warp: (t0 | t1 << 16, source-warp mask)
+// round_up(m, 4), W = the layout's sliced-ELL width, G = warps per chunk. Every
+// section before the tail sits at an offset computable from mp alone:
+//   WaveHeader (48 B)  {m, mp, q0, flags}, {nhalo, halo list, tail, hq0}, {r0, 0, 0, 0}
+//   uint2 seg[G]         per warp of the group: (t0 | t1 << 16, 0)
 //   double diag[mp]
-//   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep R)
-//   int    dep[W][mp]    0 <= d < R: ring slot; d == R: 0.0 (padding);
-//                        d > R: staged halo value d-R-1; d < 0: x[-d-1]
+//   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep -> 0.0 slot)
+//   int    dep[W][mp]    d >= 0: byte offset from the x-ring base (own row
+//                        8 (q mod R), the 0.0 slot 8R, staged value
+//                        8 (R + 1 + pos mod H)); d < 0: x[-d-1] (wave order)
 //   int exp[mp] (mailbox id or -1), (oidx[mp] if flags&2); row t's x goes to
-//   wave position r0 + t (header), so no per-row solution index is stored
+//   wave position r0 + t, so no per-row solution index is stored
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
-//   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages
-// The right-hand side arrives permuted into reordered-row order (bp[r] =
-// b[bidx[r]], one coalesced pass before the solve), so a chunk's b values are
-// one contiguous range that a second bulk copy moves next to the blob. The
-// shared-memory region of a chunk is [b: 8*mb][blob][staged halo: 8*nhalo],
-// mb = round_up(m + 1, 4); b starts one element in when r0 is odd (flags&32,
-// the copy source is rounded down to 16 bytes). The kernel addresses the region
-// from the blob start (b at -8*mb, staged halo at +bytes).
+//   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages,
+//                                  in (ELL slot, row) order of first use
+// The right-hand side arrives permuted into wave order (bp[p] = b[bidx[p]],
+// one coalesced pass before the solve), so a chunk's b values are one
+// contiguous range that a second bulk copy moves next to the blob. The
+// shared-memory region of a chunk is [b: 8*mb][blob], mb = round_up(m + 1, 4);
+// b starts one element in when r0 is odd (flags&32, the copy source is rounded
+// down to 16 bytes). Regions are placed in the byte ring by the host (span).
 struct WaveConfig {
     int ctas = 148;
     int group = 0;            // solver warps per chunk (G); 0 = auto from the rows per (CTA, level)
