@@ -58,7 +58,7 @@ void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
 constexpr int kWaveProducers = 2;                      // producer warps (chunks round robin)
-constexpr int kWaveWaiters = 3;                        // waiter warps
+constexpr int kWaveWaiters = 5;                        // waiter warps (3 could not keep up with 27-point halos)
 constexpr int kWaveRoleThreads = 32 * (kWaveProducers + kWaveWaiters);
 constexpr int kWaveCtrlBytes = 1536;                   // control block at the start of shared memory
 
