@@ -76,6 +76,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
                 throw std::invalid_argument("HEC_WAVE_G/K/RPL: no kernel for this solver shape");
         }
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
+        if (const char* e = std::getenv("HEC_WAVE_RING")) cfg.ring = std::atoi(e);           // x-ring entries (power of two)
+        if (const char* e = std::getenv("HEC_WAVE_INFLIGHT")) cfg.inflight = std::atoi(e);   // descriptor slots (power of two)
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
         const int budget = smem_optin() - 1024;  // static shared + slack
         cfg.smem_bytes = budget;
@@ -87,7 +89,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         } catch (const std::invalid_argument&) {
             ok = false;  // row order the wave layout cannot schedule: level launches
         }
-        p_ring_ = cfg.ring;
+        p_ring_ = ok ? P.ring : cfg.ring;
         p_ring_off_ = kWaveCtrlBytes;
         p_halo_ring_ = ok ? P.halo_ring : 32;
         p_buf_off_ = ok ? P.buf_off : 0;
@@ -97,9 +99,10 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_inflight_ = P.inflight;
             p_lead_ = P.lead;
             if (std::getenv("HEC_DEBUG"))
-                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d (%dx%d) rpl=%d W=%d %s grid=%dx%d max_region=%d "
+                std::fprintf(stderr, "[hec] wave n=%d chunks=%d ctas=%d warps=%d (%dx%d) rpl=%d W=%d ring=%d H=%d NS=%d %s grid=%dx%d max_region=%d "
                              "buf=%d exports=%lld deps ring=%lld global=%lld halo=%lld halo_values=%lld\n", P.n,
-                             P.chunks, P.ctas, P.warps, P.group, P.groups, P.rpl, P.max_width, P.pencils ? "pencils" : (P.strips ? "strips" : "slabs"), P.grid_nx,
+                             P.chunks, P.ctas, P.warps, P.group, P.groups, P.rpl, P.max_width, P.ring, P.halo_ring,
+                             P.inflight, P.pencils ? "pencils" : (P.strips ? "strips" : "slabs"), P.grid_nx,
                              P.grid_ny, P.max_region, p_buf_bytes_, P.exports, P.ring_deps, P.global_deps,
                              P.halo_deps, P.halo_values);
             p_smem_ = p_buf_off_ + p_buf_bytes_;
