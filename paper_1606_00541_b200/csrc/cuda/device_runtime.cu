@@ -78,6 +78,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
         if (const char* e = std::getenv("HEC_WAVE_RING")) cfg.ring = std::atoi(e);           // x-ring entries (power of two)
         if (const char* e = std::getenv("HEC_WAVE_INFLIGHT")) cfg.inflight = std::atoi(e);   // descriptor slots (power of two)
+        if (const char* e = std::getenv("HEC_WAVE_HALO_MAX")) cfg.halo_ring_max = std::atoi(e); // staged-halo ring cap
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
         const int budget = smem_optin() - 1024;  // static shared + slack
         cfg.smem_bytes = budget;

@@ -498,10 +498,12 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             }
             return worst;
         };
+        // a small x ring leaves room for a larger halo ring (27-point slabs: NS 8 -> 16, -3 %)
+        const int hmax = R <= 2048 ? 2 * cfg.halo_ring_max : cfg.halo_ring_max;
         int ns = P.inflight;
         int need = need_for(ns);
-        while (need > cfg.halo_ring_max && ns > 4) need = need_for(ns /= 2);  // NS >= 4 (kernel slot waits)
-        if (need > cfg.halo_ring_max)
+        while (need > hmax && ns > 4) need = need_for(ns /= 2);  // NS >= 4 (kernel slot waits)
+        if (need > hmax)
             throw std::invalid_argument("hec_tri_create: halo ring overflow (wave layout)");
         P.inflight = ns;
         int H = 32;
