@@ -679,7 +679,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 put_i(sec.exp, t, -1);
             }
             std::memcpy(b + sec.val, val.data(), 8 * val.size());
-            std::memcpy(b + sec.dep, dep.data(), 4 * dep.size());
+            if ((flags & 9) == 0) {  // 16-bit ring slots (byte offset / 8 < 2^16 for R + 1 + H <= 2^16)
+                for (std::size_t k = 0; k < dep.size(); ++k) {
+                    const uint16_t v = static_cast<uint16_t>(dep[k] >> 3);
+                    std::memcpy(b + sec.dep + 2 * k, &v, 2);
+                }
+            } else {
+                std::memcpy(b + sec.dep, dep.data(), 4 * dep.size());
+            }
             if (flags & 1) {
                 std::memcpy(b + sec.tptr, tptr.data(), 4 * tptr.size());
                 std::memcpy(b + sec.tval, tval.data(), 8 * tval.size());

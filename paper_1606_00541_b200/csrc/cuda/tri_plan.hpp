@@ -88,9 +88,11 @@ LevelLayout build_levels(const TriSource& s);
 //   uint2 seg[G]         per warp of the group: (t0 | t1 << 16, 0)
 //   double diag[mp]
 //   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep -> 0.0 slot)
-//   int    dep[W][mp]    d >= 0: byte offset from the x-ring base (own row
-//                        8 (q mod R), the 0.0 slot 8R, staged value
-//                        8 (R + 1 + pos mod H)); d < 0: x[-d-1] (wave order)
+//   dep[W][mp]           fast chunks (no tail, no x re-reads, flags & 9 == 0):
+//                        uint16 slot s of the x-ring array (own row q mod R,
+//                        the 0.0 slot R, staged value R + 1 + pos mod H), padded
+//                        to 16 bytes; otherwise int32 d: d >= 0 byte offset 8 s,
+//                        d < 0: x[-d-1] (wave order)
 //   int exp[mp] (mailbox id or -1), (oidx[mp] if flags&2); row t's x goes to
 //   wave position r0 + t, so no per-row solution index is stored
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
@@ -165,7 +167,7 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     b.seg = at;   at += round_up(8 * nw, 16);
     b.diag = at;  at += 8 * mp;
     b.val = at;   at += 8 * mp * w;
-    b.dep = at;   at += 4 * mp * w;
+    b.dep = at;   at += (flags & 9) == 0 ? round_up(2 * mp * w, 16) : 4 * mp * w;  // fast chunks: 16-bit ring slots
     b.exp = at;   at += 4 * mp;
     b.oidx = at;  if (flags & 2) at += 4 * mp;
     b.tptr = at;  if (flags & 1) at += 4 * round_up(mp + 1, 4);
