@@ -264,15 +264,24 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         }
         C_used = C0;
     } else {
-        // slabs: CTA c owns [c*per, (c+1)*per), warps contiguous sub-ranges
-        const int per = n > 0 ? (n + C0 - 1) / C0 : 1;
+        // slabs: CTA c owns [c*per, (c+1)*per), warps contiguous sub-ranges. On a
+        // recognised grid the slabs are whole z-planes (a plane split between two
+        // CTAs adds in-plane crossings: 27-pt 128^3 with 128 CTAs of one plane is
+        // 3 % faster than 148 CTAs of 0.86 plane)
+        int per = n > 0 ? (n + C0 - 1) / C0 : 1;
+        C_used = C0;
+        if (geo.ok && static_cast<long long>(geo.nx) * geo.ny * geo.nz == n && geo.nz >= 2) {
+            const int planes = (geo.nz + C0 - 1) / C0;
+            per = planes * geo.nx * geo.ny;
+            C_used = (geo.nz + planes - 1) / planes;
+        }
+        const int Cs = C_used;
         const int per_w = (per + NW - 1) / NW;
 #pragma omp parallel for schedule(static)
         for (int i = 0; i < n; ++i) {
-            owner_i[i] = std::min(i / per, C0 - 1);
+            owner_i[i] = std::min(i / per, Cs - 1);
             warp_i[i] = std::min((i - owner_i[i] * per) / per_w, NW - 1);
         }
-        C_used = C0;
     }
     P.ctas = C_used;
     const int C = C_used;
