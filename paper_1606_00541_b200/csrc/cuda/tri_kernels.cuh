@@ -39,20 +39,20 @@ struct WaveArgs {
     int ctas;
     int inflight;                // descriptor slots (power of two <= 32)
     int inflight_log2;
-    int lead;                    // max chunks a warp runs ahead of the slowest warp
+    int lead;                    // (informational: 1, chunks complete in order)
     int ring;                    // x ring entries (power of two)
     int halo_ring;               // H: staged-halo ring entries, behind the x ring
     int ring_off;                // shared-memory byte offsets
     int buf_off;
     int buf_bytes;
-    int spin_ns;                 // back-off inside the solvers' shared-memory spins (HEC_WAVE_SPIN_NS)
+    int spin_ns;                 // back-off between the waiters' mailbox polls (HEC_WAVE_SPIN_NS, 0 = off)
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 
 void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
-// kernel for sliced-ELL width W (one of 1-8, 10, 13, 16; nullptr otherwise):
-// 16 solver warps with one row per lane, or one solver warp with rpl (2, 4, 8)
-// rows per lane
+// kernel for sliced-ELL width W (one of 1-8, 10, 13, 16) and solver shape
+// (group warps G x groups K x rpl rows per lane, see wave_inst.cuh); nullptr
+// when that combination is not instantiated
 void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);

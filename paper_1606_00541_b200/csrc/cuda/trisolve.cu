@@ -10,18 +10,14 @@
 // Two strategies:
 //  * k_level_rows   one launch per level, thread per reordered row (baseline;
 //                   the reference's level barrier becomes a kernel boundary).
-//  * k_wave         persistent wavefront, one CTA per SM (tri_plan.hpp). CTA c
-//                   owns a contiguous block of lower-frame rows, each solver
-//                   warp a fixed slice of it. Warp roles: 0 = producer (byte-
-//                   ring allocation + cp.async.bulk of chunk blobs into shared
-//                   memory), 1..kWaveWaiters = waiters (cp.async gather of b,
-//                   polling of the epoch-tagged mailboxes that carry values
-//                   from lower CTAs), the rest = solvers. The reference's
-//                   per-level barrier becomes dataflow: a warp starts its part
-//                   of level k as soon as the warps it reads from finished
-//                   level k-1 (shared-memory progress counters) and the
-//                   foreign values are staged; no grid or CTA barrier.
-
+//  * k_wave         persistent wavefront, one CTA per SM (wave_kernel.cuh,
+//                   layout in tri_plan.hpp). Warp roles: 2 producers (bulk
+//                   copies of chunk blobs into a host-placed shared-memory byte
+//                   ring), 5 waiters (poll the epoch-tagged mailboxes of values
+//                   from other CTAs, stage them, publish the chunk on an
+//                   mbarrier), K groups of G solver warps taking the chunks round
+//                   robin with a named-barrier handoff. The reference's per-level
+//                   barrier becomes dataflow; no grid barrier.
 
 #include <cuda_runtime.h>
 
