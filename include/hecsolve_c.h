@@ -72,6 +72,11 @@ typedef struct {
     long long device_bytes;
     double alg_bytes;    /* 12 nnz_T + 20 n                   */
     double predicted_us; /* cost-model critical path of one solve               */
+    /* PIPELINE layout actually built (diagnostics; -1 / 0 for LEVELS) */
+    int layout;          /* 0 slabs, 1 z-pencils (recognised grid), 2 strips      */
+    int group, groups, rows_per_lane; /* solver shape G x K x RPL               */
+    int width;           /* sliced-ELL width W of the device blob                */
+    int ring, halo_ring, inflight;    /* shared-memory rings, descriptor slots  */
 } hec_tri_info;
 
 typedef struct hec_tri* hec_tri_t;
@@ -171,12 +176,26 @@ int hec_precond_apply_host(hec_precond_t m, const double* r, double* x);
 int hec_precond_query(hec_precond_t m, hec_tri_info* l_info, hec_tri_info* u_info);
 int hec_precond_destroy(hec_precond_t m);
 
-/* CSR SpMV on the device: y = A x, row sums in ascending column order
- * (bitwise equal to spmv_csr, proj/src/csr.cpp:43-57). */
+/* HEC SpMV on the device: y = A x over column-major ELL slots (256-byte
+ * aligned columns, vectorised coalesced loads) plus a CSR remainder staged
+ * through shared memory per warp.
+ * hec_spmv_create: from CSR, split as hec_from_csr(a, false, automatic) with
+ *   padding skipped -- row sums in storage order, bitwise equal to spmv_csr
+ *   (proj/src/csr.cpp:43-57).
+ * hec_spmv_create_hec: from a reference HecMatrix's fields (hec.hpp:13-46:
+ *   ell.{width, col_indices[width*n_rows], values} column-major, csr.{row_offsets,
+ *   col_indices, values}); bitwise equal to spmv_hec (proj/src/hec.cpp:88-108),
+ *   padding slots multiplied as the reference does.
+ * hec_spmv_residual: y = b - A x with A x summed as above (gmres.cpp:19-24). */
 typedef struct hec_spmv* hec_spmv_t;
 int hec_spmv_create(int n_rows, int n_cols, const int* row_offsets, const int* cols,
                     const double* vals, hec_spmv_t* out);
+int hec_spmv_create_hec(int n_rows, int n_cols, int ell_width, const int* ell_cols,
+                        const double* ell_vals, const int* csr_row_offsets, const int* csr_cols,
+                        const double* csr_vals, hec_spmv_t* out);
 int hec_spmv_run(hec_spmv_t a, const double* x_dev, double* y_dev, void* stream);
+int hec_spmv_residual(hec_spmv_t a, const double* b_dev, const double* x_dev, double* y_dev,
+                      void* stream);
 int hec_spmv_run_host(hec_spmv_t a, const double* x, double* y);
 int hec_spmv_destroy(hec_spmv_t a);
 
@@ -231,7 +250,25 @@ int hec_csr_from_triples(int n_rows, int n_cols, long long count, const int* row
 int hec_csr_view(hec_csr_t a, int* n_rows, int* n_cols, long long* nnz,
                  const int** row_offsets, const int** cols, const double** vals);
 int hec_csr_destroy(hec_csr_t a);
+/* hec::spmv_csr (csr.hpp:35-36): y = A x on the device (host vectors). */
 int hec_csr_spmv_host(hec_csr_t a, const double* x, double* y, int workers);
+
+/* hec::hec_from_csr (hec.hpp:48, hec.cpp:28-86) and hec::spmv_hec (hec.hpp:52-53,
+ * on the device). width_mode 0 = automatic (median), 1 = fixed `width`. */
+typedef struct hec_hec* hec_hec_t;   /* owns a hec::HecMatrix */
+typedef struct {
+    int n_rows, n_cols, ell_width;
+    const int* ell_cols;       /* [ell_width * n_rows], slot k of row i at k*n_rows+i */
+    const double* ell_vals;
+    const int* csr_row_offsets; /* [n_rows + 1] */
+    const int* csr_cols;
+    const double* csr_vals;
+    long long csr_nnz;
+} hec_hec_view;
+int hec_hec_from_csr(hec_csr_t a, int triangular, int width_mode, int width, hec_hec_t* out);
+int hec_hec_view_get(hec_hec_t h, hec_hec_view* v);
+int hec_hec_spmv_host(hec_hec_t h, const double* x, double* y, int workers);
+int hec_hec_destroy(hec_hec_t h);
 
 int hec_gen_poisson7(int nx, int ny, int nz, hec_csr_t* out);
 int hec_gen_poisson27(int nx, int ny, int nz, hec_csr_t* out);

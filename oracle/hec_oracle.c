@@ -291,3 +291,105 @@ double orc_dot(int n, const double* a, const double* b) {
     for (int i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
 }
+
+/* Generators of the configs the reference has no generator for (SURVEY.md
+ * 8(d) C2/C3 definitions; the reference's gen_poisson7 pattern, poisson.cpp:8-43,
+ * extended). Input data only: used by the golden script and bench.py's
+ * reference arm so neither needs the product library. */
+
+/* 27-point: diagonal 26, -1 for every existing neighbour, ascending columns. */
+long long orc_poisson27(int nx, int ny, int nz, int* rp, int* ci, double* v) {
+    long long at = 0, id = 0;
+    if (rp) rp[0] = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x, ++id) {
+                for (int dz = -1; dz <= 1; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (z + dz < 0 || z + dz >= nz || y + dy < 0 || y + dy >= ny || x + dx < 0 ||
+                                x + dx >= nx)
+                                continue;
+                            if (rp) {
+                                ci[at] = (int)(id + dx + (long long)nx * (dy + (long long)ny * dz));
+                                v[at] = (dx == 0 && dy == 0 && dz == 0) ? 26.0 : -1.0;
+                            }
+                            ++at;
+                        }
+                if (rp) rp[id + 1] = (int)at;
+            }
+    return at;
+}
+
+/* std::mt19937_64 (the C++ standard's parameters), for gen_reservoir7's draws. */
+typedef struct { unsigned long long mt[312]; int i; } orc_mt64;
+static void mt64_seed(orc_mt64* s, unsigned long long seed) {
+    s->mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+        s->mt[i] = 6364136223846793005ULL * (s->mt[i - 1] ^ (s->mt[i - 1] >> 62)) + (unsigned long long)i;
+    s->i = 312;
+}
+static unsigned long long mt64_next(orc_mt64* s) {
+    if (s->i >= 312) {
+        for (int k = 0; k < 312; ++k) {
+            const unsigned long long y = (s->mt[k] & 0xFFFFFFFF80000000ULL) | (s->mt[(k + 1) % 312] & 0x7FFFFFFFULL);
+            s->mt[k] = s->mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+        }
+        s->i = 0;
+    }
+    unsigned long long x = s->mt[s->i++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= x >> 43;
+    return x;
+}
+
+/* Reservoir-style 7-point: k_c = 10^(sigma (2u-1)), u =
+ * (mt19937_64() >> 11) 2^-53 in cell order; vertical faces use kz_ratio k;
+ * interior face T = 2ab/(a+b), a boundary face adds the cell's own k to the
+ * diagonal; A_ii = sum of the six T, A_ij = -T. Pattern = gen_poisson7. */
+long long orc_reservoir7(int nx, int ny, int nz, double sigma, double kz_ratio, unsigned long long seed, int* rp,
+                         int* ci, double* v) {
+    const long long n = (long long)nx * ny * nz;
+    const long long nnz = 7 * n - 2 * ((long long)nx * ny + (long long)ny * nz + (long long)nx * nz);
+    if (!rp) return nnz;
+    double* k = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    orc_mt64* s = (orc_mt64*)malloc(sizeof(orc_mt64));
+    mt64_seed(s, seed);
+    for (long long c = 0; c < n; ++c) {
+        const double u = (double)(mt64_next(s) >> 11) * 0x1.0p-53;
+        k[c] = pow(10.0, sigma * (2.0 * u - 1.0));
+    }
+    free(s);
+    const long long plane = (long long)nx * ny;
+    long long at = 0, id = 0;
+    rp[0] = 0;
+    for (int z = 0; z < nz; ++z)
+        for (int y = 0; y < ny; ++y)
+            for (int x = 0; x < nx; ++x, ++id) {
+                const double kh = k[id], kv = kz_ratio * k[id];
+                const int has[6] = {z > 0, y > 0, x > 0, x + 1 < nx, y + 1 < ny, z + 1 < nz};
+                const long long nb[6] = {id - plane, id - nx, id - 1, id + 1, id + nx, id + plane};
+                double t[6], d = 0.0;
+                for (int f = 0; f < 6; ++f) {
+                    const int vert = (f == 0 || f == 5);
+                    const double own = vert ? kv : kh;
+                    if (has[f]) {
+                        const double other = vert ? kz_ratio * k[nb[f]] : k[nb[f]];
+                        t[f] = 2.0 * own * other / (own + other);
+                    } else {
+                        t[f] = own;
+                    }
+                }
+                for (int f = 0; f < 6; ++f) d += t[f];
+                for (int f = 0; f < 3; ++f)
+                    if (has[f]) { ci[at] = (int)nb[f]; v[at++] = -t[f]; }
+                ci[at] = (int)id; v[at++] = d;
+                for (int f = 3; f < 6; ++f)
+                    if (has[f]) { ci[at] = (int)nb[f]; v[at++] = -t[f]; }
+                rp[id + 1] = (int)at;
+            }
+    free(k);
+    return nnz;
+}

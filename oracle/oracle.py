@@ -86,6 +86,10 @@ class Oracle:
         L.orc_backward.restype = C.c_int
         L.orc_ilu0_inplace.restype = C.c_int
         L.orc_poisson7.restype = C.c_longlong
+        L.orc_poisson27.restype = C.c_longlong
+        L.orc_reservoir7.restype = C.c_longlong
+        L.orc_reservoir7.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_ulonglong,
+                                     P_int, P_int, P_dbl]
         L.orc_dot.restype = C.c_double
 
     # reference poisson.cpp:8-43
@@ -94,6 +98,22 @@ class Oracle:
         n = nx * ny * nz
         rp, ci, v = np.empty(n + 1, I32), np.empty(nnz, I32), np.empty(nnz, F64)
         self.lib.orc_poisson7(nx, ny, nz, _pi(rp), _pi(ci), _pd(v))
+        return Csr(n, n, rp, ci, v)
+
+    # SURVEY.md 8(d) C2 (27-point Poisson, the 7-point pattern of poisson.cpp:8-43 extended)
+    def poisson27(self, nx, ny, nz) -> Csr:
+        nnz = self.lib.orc_poisson27(nx, ny, nz, None, None, None)
+        n = nx * ny * nz
+        rp, ci, v = np.empty(n + 1, I32), np.empty(nnz, I32), np.empty(nnz, F64)
+        self.lib.orc_poisson27(nx, ny, nz, _pi(rp), _pi(ci), _pd(v))
+        return Csr(n, n, rp, ci, v)
+
+    # SURVEY.md 8(d) C3 (heterogeneous reservoir 7-point)
+    def reservoir7(self, nx, ny, nz, sigma=3.0, kz_ratio=0.1, seed=1606) -> Csr:
+        nnz = self.lib.orc_reservoir7(nx, ny, nz, sigma, kz_ratio, seed, None, None, None)
+        n = nx * ny * nz
+        rp, ci, v = np.empty(n + 1, I32), np.empty(nnz, I32), np.empty(nnz, F64)
+        self.lib.orc_reservoir7(nx, ny, nz, sigma, kz_ratio, seed, _pi(rp), _pi(ci), _pd(v))
         return Csr(n, n, rp, ci, v)
 
     # reference triangular.cpp:43-63
@@ -229,6 +249,7 @@ class Reference:
                                   C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         L.ref_gmres.argtypes = [C.c_int, P_int, P_int, P_dbl, P_dbl, C.c_void_p, C.c_int, C.c_int, C.c_double,
                                 C.c_double, C.c_int, P_dbl, P_dbl]
+        L.ref_precond_single.argtypes = [C.c_int, P_int, P_int, P_dbl, P_int, P_int, P_dbl, C.POINTER(C.c_void_p)]
         L.ref_ilu.argtypes = [C.c_int, P_int, P_int, P_dbl, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_void_p)]
         L.ref_prepared_from_arrays.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, P_int, P_int, P_int, P_int,
                                                C.c_int, P_int, P_dbl, P_int, P_int, P_dbl, C.POINTER(C.c_void_p)]
@@ -365,6 +386,11 @@ class Reference:
         wm, w = (1, fixed_width) if fixed_width is not None else (0, 0)
         return self._bag(self.lib.ref_precond, a.n, _pi(a.rp), _pi(a.ci), _pd(a.v),
                          {"bilu0": 0, "bilut": 1, "ras": 2}[kind], blocks, overlap, p, tol, wm, w)
+
+    def precond_single(self, l: Csr, u: Csr):
+        """One block holding the given factors (ILU(k) has no PrecondKind)."""
+        return self._bag(self.lib.ref_precond_single, l.n, _pi(l.rp), _pi(l.ci), _pd(l.v), _pi(u.rp), _pi(u.ci),
+                         _pd(u.v))
 
     def apply(self, bp_bag, r, workers=1) -> np.ndarray:
         r = np.ascontiguousarray(r, F64)

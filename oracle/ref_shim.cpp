@@ -277,6 +277,35 @@ __attribute__((visibility("default"))) int ref_precond(int n, const int* rp, con
     });
 }
 
+// A single-block BlockPreconditioner holding the given factors (the hand
+// assembly SURVEY.md 8(b) describes for ILU(k), which PrecondKind lacks):
+// apply() reads only n, partition.n_parts, extended_parts, offsets,
+// restriction and prepared_l/u (precond.cpp:119-145).
+__attribute__((visibility("default"))) int ref_precond_single(int n, const int* lrp, const int* lci, const double* lv,
+                                                              const int* urp, const int* uci, const double* uv,
+                                                              void** out) {
+    return guard([&] {
+        auto b = std::make_unique<Bag>();
+        auto m = std::make_shared<hecref::BlockPreconditioner>();
+        m->kind = hecref::PrecondKind::bilu0;
+        m->n = n;
+        m->partition.n = n;
+        m->partition.n_parts = 1;
+        m->partition.part_of.assign(n, 0);
+        std::vector<int> rows(n);
+        for (int i = 0; i < n; ++i) rows[i] = i;
+        m->partition.parts = {rows};
+        m->extended_parts = {rows};
+        m->restriction = {std::vector<char>(n, 1)};
+        m->offsets = {0, n};
+        const hecref::CsrMatrix l = csr_in(n, n, lrp, lci, lv), u = csr_in(n, n, urp, uci, uv);
+        m->prepared_l = hecref::prepare_lower(l);
+        m->prepared_u = hecref::prepare_upper(u);
+        b->bp = m;
+        *out = b.release();
+    });
+}
+
 __attribute__((visibility("default"))) int ref_apply(void* bp, const double* r, double* x, int workers) {
     return guard([&] {
         const Bag* b = static_cast<Bag*>(bp);

@@ -34,7 +34,9 @@ class TriOptions(C.Structure):
 class TriInfo(C.Structure):
     _fields_ = [("n", c_int), ("nlev", c_int), ("strategy", c_int), ("ctas", c_int),
                 ("threads", c_int), ("chunks", c_int), ("nnz", c_ll), ("device_bytes", c_ll),
-                ("alg_bytes", c_dbl), ("predicted_us", c_dbl)]
+                ("alg_bytes", c_dbl), ("predicted_us", c_dbl), ("layout", c_int), ("group", c_int),
+                ("groups", c_int), ("rows_per_lane", c_int), ("width", c_int), ("ring", c_int),
+                ("halo_ring", c_int), ("inflight", c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -47,6 +49,12 @@ class GmresConfig(C.Structure):
 class GmresReport(C.Structure):
     _fields_ = [("converged", c_int), ("iterations", c_int), ("final_relative_residual", c_dbl),
                 ("solve_seconds", c_dbl), ("n_inner", c_int)]
+
+
+class HecView(C.Structure):
+    _fields_ = [("n_rows", c_int), ("n_cols", c_int), ("ell_width", c_int), ("ell_cols", P_int),
+                ("ell_vals", P_dbl), ("csr_row_offsets", P_int), ("csr_cols", P_int), ("csr_vals", P_dbl),
+                ("csr_nnz", c_ll)]
 
 
 class PrepView(C.Structure):

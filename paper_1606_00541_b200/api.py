@@ -271,6 +271,35 @@ class HecMatrix:
     csr_row_offsets: np.ndarray
     csr_col_indices: np.ndarray
     csr_values: np.ndarray
+    _handle: object = None  # owning hec_hec_t when built by hec_from_csr
+
+    def __del__(self):
+        if self._handle is not None:
+            lib.hec_hec_destroy(self._handle)
+            self._handle = None
+
+
+def hec_from_csr(a: CsrMatrix, triangular: bool = False, policy: "Optional[WidthPolicy]" = None) -> HecMatrix:
+    """hec::hec_from_csr (reference hec.hpp:48, hec.cpp:28-86), host setup."""
+    mode, width = (policy or WidthPolicy()).c_args()
+    h = C.c_void_p()
+    check(lib.hec_hec_from_csr(a.handle, int(bool(triangular)), mode, width, C.byref(h)))
+    v = L.HecView()
+    check(lib.hec_hec_view_get(h, C.byref(v)))
+    n, w = v.n_rows, v.ell_width
+    return HecMatrix(n, v.n_cols, EllMatrix(n, w, _view(v.ell_cols, w * n, _i32), _view(v.ell_vals, w * n, _f64)),
+                     _view(v.csr_row_offsets, n + 1, _i32), _view(v.csr_cols, v.csr_nnz, _i32),
+                     _view(v.csr_vals, v.csr_nnz, _f64), h)
+
+
+def spmv_hec(h: HecMatrix, x, workers: int = 1) -> np.ndarray:
+    """hec::spmv_hec on the B200 (reference hec.cpp:88-108); h from hec_from_csr."""
+    if h._handle is None:
+        raise ValueError("spmv_hec: HecMatrix not built by hec_from_csr")
+    xv = _f64_vec(x, h.n_cols, "spmv_hec")
+    y = np.empty(h.n_rows, dtype=_f64)
+    check(lib.hec_hec_spmv_host(h._handle, _p_dbl(xv), _p_dbl(y), workers))
+    return y
 
 
 class PreparedTriangular:
@@ -503,12 +532,33 @@ class DevicePrecond:
 
 
 class DeviceSpmv:
-    def __init__(self, a: CsrMatrix):
+    """hec_spmv_t: the device HEC SpMV (from CSR: bitwise spmv_csr; from_hec: bitwise spmv_hec)."""
+
+    def __init__(self, a: Optional[CsrMatrix], _h=None, _dims=None):
+        if a is None:
+            self._h = _h
+            self.n_rows, self.n_cols = _dims
+            return
         self.n_rows, self.n_cols = a.n_rows, a.n_cols
         h = C.c_void_p()
         check(lib.hec_spmv_create(a.n_rows, a.n_cols, _p_int(a.row_offsets), _p_int(a.col_indices),
                                   _p_dbl(a.values), C.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_hec(cls, m: HecMatrix) -> "DeviceSpmv":
+        h = C.c_void_p()
+        e = m.ell
+        check(lib.hec_spmv_create_hec(m.n_rows, m.n_cols, e.width, _p_int(e.col_indices), _p_dbl(e.values),
+                                      _p_int(m.csr_row_offsets), _p_int(m.csr_col_indices),
+                                      _p_dbl(m.csr_values), C.byref(h)))
+        return cls(None, h, (m.n_rows, m.n_cols))
+
+    def residual(self, b_dev, x_dev, y_dev, stream=None):
+        """y = b - A x"""
+        check(lib.hec_spmv_residual(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(x_dev)),
+                                    C.c_void_p(_ptr(y_dev)),
+                                    C.c_void_p(_stream(stream)) if stream is not None else None))
 
     def run(self, x_dev, y_dev, stream=None):
         check(lib.hec_spmv_run(self._h, C.c_void_p(_ptr(x_dev)), C.c_void_p(_ptr(y_dev)),

@@ -47,6 +47,9 @@ struct hec_bp {
 struct hec_krylov {
     std::unique_ptr<hec::dev::KrylovOps> impl;
 };
+struct hec_hec {
+    hec::HecMatrix m;
+};
 struct hec_partition {
     int n = 0, parts = 0;
     std::vector<int> part_of, ext_offsets, ext_rows;
@@ -270,6 +273,14 @@ void fill_info(const hec::dev::TriStats& s, hec_tri_info* info) {
     info->device_bytes = s.device_bytes;
     info->alg_bytes = s.alg_bytes;
     info->predicted_us = s.predicted_us;
+    info->layout = s.layout;
+    info->group = s.group;
+    info->groups = s.groups;
+    info->rows_per_lane = s.rpl;
+    info->width = s.width;
+    info->ring = s.ring;
+    info->halo_ring = s.halo_ring;
+    info->inflight = s.slots;
 }
 
 hec::WidthPolicy policy_of(int mode, int width) {
@@ -512,6 +523,25 @@ int hec_spmv_create(int n_rows, int n_cols, const int* row_offsets, const int* c
     });
 }
 
+int hec_spmv_create_hec(int n_rows, int n_cols, int ell_width, const int* ell_cols, const double* ell_vals,
+                        const int* csr_row_offsets, const int* csr_cols, const double* csr_vals, hec_spmv_t* out) {
+    return guarded([&] {
+        need(out, "hec_spmv_create_hec");
+        if (n_rows > 0) need(csr_row_offsets, "hec_spmv_create_hec");
+        auto h = std::make_unique<hec_spmv>();
+        h->impl = std::make_unique<hec::dev::DeviceSpmv>(n_rows, n_cols, ell_width, ell_cols, ell_vals,
+                                                         csr_row_offsets, csr_cols, csr_vals);
+        *out = h.release();
+    });
+}
+
+int hec_spmv_residual(hec_spmv_t a, const double* b_dev, const double* x_dev, double* y_dev, void* stream) {
+    return guarded([&] {
+        need(a, "hec_spmv_residual");
+        a->impl->residual(b_dev, x_dev, y_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int hec_spmv_run(hec_spmv_t a, const double* x_dev, double* y_dev, void* stream) {
     return guarded([&] {
         need(a, "hec_spmv_run");
@@ -607,6 +637,46 @@ int hec_csr_spmv_host(hec_csr_t a, const double* x, double* y, int workers) {
         const std::vector<double> yv = hec::spmv_csr(a->m, xv, workers);
         std::copy(yv.begin(), yv.end(), y);
     });
+}
+
+int hec_hec_from_csr(hec_csr_t a, int triangular, int width_mode, int width, hec_hec_t* out) {
+    return guarded([&] {
+        need(a, "hec_hec_from_csr");
+        need(out, "hec_hec_from_csr");
+        auto h = std::make_unique<hec_hec>();
+        h->m = hec::hec_from_csr(a->m, triangular != 0, policy_of(width_mode, width));
+        *out = h.release();
+    });
+}
+
+int hec_hec_view_get(hec_hec_t h, hec_hec_view* v) {
+    return guarded([&] {
+        need(h, "hec_hec_view_get");
+        need(v, "hec_hec_view_get");
+        const hec::HecMatrix& m = h->m;
+        v->n_rows = m.n_rows;
+        v->n_cols = m.n_cols;
+        v->ell_width = m.ell.width;
+        v->ell_cols = m.ell.col_indices.data();
+        v->ell_vals = m.ell.values.data();
+        v->csr_row_offsets = m.csr.row_offsets.data();
+        v->csr_cols = m.csr.col_indices.data();
+        v->csr_vals = m.csr.values.data();
+        v->csr_nnz = static_cast<long long>(m.csr.col_indices.size());
+    });
+}
+
+int hec_hec_spmv_host(hec_hec_t h, const double* x, double* y, int workers) {
+    return guarded([&] {
+        need(h, "hec_hec_spmv_host");
+        std::vector<double> xv(x, x + h->m.n_cols);
+        const std::vector<double> yv = hec::spmv_hec(h->m, xv, workers);
+        std::copy(yv.begin(), yv.end(), y);
+    });
+}
+
+int hec_hec_destroy(hec_hec_t h) {
+    return guarded([&] { delete h; });
 }
 
 #define HEC_WRAP_GEN(expr)                     \

@@ -128,6 +128,13 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             if (!p_kernel_) throw std::invalid_argument("hec_tri_create: no wave kernel for this width");
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
+            stats_.layout = P.pencils ? 1 : (P.strips ? 2 : 0);
+            stats_.group = P.group;
+            stats_.groups = P.groups;
+            stats_.rpl = P.rpl;
+            stats_.width = P.max_width;
+            stats_.ring = P.ring;
+            stats_.halo_ring = P.halo_ring;
             stats_.device_bytes = static_cast<long long>(P.blob.size() + 4 * P.span.size() + 4 * P.cta_chunk0.size() +
                                                          4 * P.bidx.size() + 16 * P.exports);
         } else {
@@ -395,61 +402,6 @@ void DevicePrecond::apply_host(const double* r, double* x) {
     apply(h_r_.p, h_x_.p, h_stream_);
     HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, sizeof(double) * n_out_, cudaMemcpyDeviceToHost, h_stream_));
     HEC_CUDA(cudaStreamSynchronize(h_stream_));
-}
-
-// ----------------------------------------------------------- DeviceSpmv ----
-// Thread per row, ascending-column accumulation with separately rounded
-// multiply and add: bitwise equal to the reference's spmv_csr
-// (proj/src/csr.cpp:49-55).
-__global__ void k_spmv_csr(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                           const double* __restrict__ v, const double* x, double* y) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
-    y[i] = s;
-}
-
-// y = b - A x with A x accumulated exactly as above, then one subtraction
-// (reference residual(), proj/src/gmres.cpp:19-24).
-__global__ void k_residual_csr(int n, const int* __restrict__ rp, const int* __restrict__ ci,
-                               const double* __restrict__ v, const double* b, const double* x, double* y) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double s = 0.0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
-    y[i] = __dsub_rn(b[i], s);
-}
-
-DeviceSpmv::DeviceSpmv(int n_rows, int n_cols, const int* rp, const int* ci, const double* v)
-    : n_rows_(n_rows), n_cols_(n_cols) {
-    require_device();
-    if (n_rows < 0 || n_cols < 0) throw std::invalid_argument("hec_spmv_create: negative dimension");
-    nnz_ = n_rows > 0 ? rp[n_rows] : 0;
-    rp_.upload(rp, static_cast<std::size_t>(n_rows) + 1);
-    ci_.upload(ci, static_cast<std::size_t>(nnz_));
-    v_.upload(v, static_cast<std::size_t>(nnz_));
-}
-
-void DeviceSpmv::run(const double* x, double* y, cudaStream_t st) const {
-    if (n_rows_ == 0) return;
-    k_spmv_csr<<<(n_rows_ + 255) / 256, 256, 0, st>>>(n_rows_, rp_.p, ci_.p, v_.p, x, y);
-    HEC_CUDA(cudaGetLastError());
-}
-
-void DeviceSpmv::residual(const double* b, const double* x, double* y, cudaStream_t st) const {
-    if (n_rows_ == 0) return;
-    k_residual_csr<<<(n_rows_ + 255) / 256, 256, 0, st>>>(n_rows_, rp_.p, ci_.p, v_.p, b, x, y);
-    HEC_CUDA(cudaGetLastError());
-}
-
-void DeviceSpmv::run_host(const double* x, double* y) {
-    std::lock_guard<std::mutex> g(mu_);
-    if (h_x_.count < static_cast<std::size_t>(std::max(n_cols_, 1))) h_x_.alloc(std::max(n_cols_, 1));
-    if (h_y_.count < static_cast<std::size_t>(std::max(n_rows_, 1))) h_y_.alloc(std::max(n_rows_, 1));
-    HEC_CUDA(cudaMemcpy(h_x_.p, x, sizeof(double) * n_cols_, cudaMemcpyHostToDevice));
-    run(h_x_.p, h_y_.p, nullptr);
-    HEC_CUDA(cudaMemcpy(y, h_y_.p, sizeof(double) * n_rows_, cudaMemcpyDeviceToHost));
 }
 
 }  // namespace hec::dev

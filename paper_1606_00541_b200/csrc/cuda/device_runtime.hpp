@@ -66,6 +66,7 @@ struct TriOptions {
 
 struct TriStats {
     int n = 0, nlev = 0, strategy = 0, ctas = 0, threads = 0, chunks = 0, slots = 0;
+    int layout = -1, group = 0, groups = 0, rpl = 0, width = 0, ring = 0, halo_ring = 0;
     long long nnz = 0, device_bytes = 0;
     double alg_bytes = 0.0, predicted_us = 0.0;
 };
@@ -177,9 +178,15 @@ public:
     ~DevicePrecond();
 };
 
+// Device HEC SpMV (spmv_hec.cu): column-major ELL slots + CSR remainder.
 class DeviceSpmv {
 public:
+    // From CSR: split like hec_from_csr(a, false, automatic), padding skipped
+    // (bitwise spmv_csr, proj/src/csr.cpp:43-57).
     DeviceSpmv(int n_rows, int n_cols, const int* rp, const int* ci, const double* v);
+    // From a reference HecMatrix (bitwise spmv_hec, proj/src/hec.cpp:88-108).
+    DeviceSpmv(int n_rows, int n_cols, int width, const int* ell_cols, const double* ell_vals, const int* csr_rp,
+               const int* csr_ci, const double* csr_v);
     void run(const double* x, double* y, cudaStream_t st) const;
     // y = b - A x (fused residual)
     void residual(const double* b, const double* x, double* y, cudaStream_t st) const;
@@ -187,14 +194,27 @@ public:
     int n_rows() const { return n_rows_; }
     int n_cols() const { return n_cols_; }
     long long nnz() const { return nnz_; }
+    int ell_width() const { return w_; }
+    // algorithmic bytes of one product: 12 nnz + 4 (n+1) + 16 n
+    double alg_bytes() const { return 12.0 * nnz_ + 4.0 * (n_rows_ + 1) + 16.0 * n_rows_; }
 
 private:
-    int n_rows_ = 0, n_cols_ = 0;
+    void upload(int w, const std::vector<int>& col, const std::vector<double>& val, const std::vector<int>& rp,
+                const std::vector<int>& ci, const std::vector<double>& v);
+    void launch(const double* x, const double* b, double* y, cudaStream_t st) const;
+    int n_rows_ = 0, n_cols_ = 0, w_ = 0, ld_ = 0;
+    bool has_rem_ = false;
     long long nnz_ = 0;
-    DevBuf<int> rp_, ci_;
-    DevBuf<double> v_;
+    DevBuf<int> ell_col_, rem_rp_, rem_ci_;
+    DevBuf<double> ell_val_, rem_v_;
     std::mutex mu_;
     DevBuf<double> h_x_, h_y_;
 };
+
+// One-shot products with host vectors (the drop-in hec::spmv_csr / spmv_hec).
+std::vector<double> spmv_csr_device(int n_rows, int n_cols, const int* rp, const int* ci, const double* v,
+                                    const double* x);
+std::vector<double> spmv_hec_device(int n_rows, int n_cols, int width, const int* ell_cols, const double* ell_vals,
+                                    const int* csr_rp, const int* csr_ci, const double* csr_v, const double* x);
 
 }  // namespace hec::dev
