@@ -109,7 +109,9 @@ _sig("hec_precond_apply_host", c_int, c_void_p, P_dbl, P_dbl)
 _sig("hec_precond_query", c_int, c_void_p, C.POINTER(TriInfo), C.POINTER(TriInfo))
 _sig("hec_precond_destroy", c_int, c_void_p)
 _sig("hec_spmv_create", c_int, c_int, c_int, P_int, P_int, P_dbl, C.POINTER(c_void_p))
+_sig("hec_spmv_create_hec", c_int, c_int, c_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl, C.POINTER(c_void_p))
 _sig("hec_spmv_run", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_spmv_residual", c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p)
 _sig("hec_spmv_run_host", c_int, c_void_p, P_dbl, P_dbl)
 _sig("hec_spmv_destroy", c_int, c_void_p)
 _sig("hec_gmres_solve", c_int, c_void_p, c_void_p, P_dbl, C.POINTER(GmresConfig), P_dbl,
@@ -120,6 +122,10 @@ _sig("hec_csr_from_triples", c_int, c_int, c_int, c_ll, P_int, P_int, P_dbl, C.P
 _sig("hec_csr_view", c_int, c_void_p, P_int, P_int, C.POINTER(c_ll), PP_int, PP_int, PP_dbl)
 _sig("hec_csr_destroy", c_int, c_void_p)
 _sig("hec_csr_spmv_host", c_int, c_void_p, P_dbl, P_dbl, c_int)
+_sig("hec_hec_from_csr", c_int, c_void_p, c_int, c_int, c_int, C.POINTER(c_void_p))
+_sig("hec_hec_view_get", c_int, c_void_p, C.POINTER(HecView))
+_sig("hec_hec_spmv_host", c_int, c_void_p, P_dbl, P_dbl, c_int)
+_sig("hec_hec_destroy", c_int, c_void_p)
 _sig("hec_gen_poisson7", c_int, c_int, c_int, c_int, C.POINTER(c_void_p))
 _sig("hec_gen_poisson27", c_int, c_int, c_int, c_int, C.POINTER(c_void_p))
 _sig("hec_gen_reservoir7", c_int, c_int, c_int, c_int, c_dbl, c_dbl, C.c_uint64, C.POINTER(c_void_p))
@@ -158,9 +164,10 @@ EXPORTED = [
     "hec_precond_query", "hec_krylov_create", "hec_krylov_mgs", "hec_krylov_scale", "hec_krylov_combine",
     "hec_krylov_add", "hec_krylov_sqrt", "hec_krylov_destroy", "hec_csr_submatrix", "hec_partition_create",
     "hec_partition_view", "hec_partition_destroy",
-    "hec_precond_destroy", "hec_spmv_create", "hec_spmv_run", "hec_spmv_run_host", "hec_spmv_destroy",
+    "hec_precond_destroy", "hec_spmv_create", "hec_spmv_create_hec", "hec_spmv_residual", "hec_spmv_run", "hec_spmv_run_host", "hec_spmv_destroy",
     "hec_gmres_solve", "hec_csr_create", "hec_csr_from_triples", "hec_csr_view", "hec_csr_destroy",
-    "hec_csr_spmv_host", "hec_gen_poisson7", "hec_gen_poisson27", "hec_gen_reservoir7",
+    "hec_csr_spmv_host", "hec_hec_from_csr", "hec_hec_view_get", "hec_hec_spmv_host", "hec_hec_destroy",
+    "hec_gen_poisson7", "hec_gen_poisson27", "hec_gen_reservoir7",
     "hec_permute_symmetric", "hec_random_ordering", "hec_rcm_ordering", "hec_ilu0", "hec_ilu_k", "hec_ilut",
     "hec_prepare", "hec_prep_view_get", "hec_prep_solve_host", "hec_prep_device", "hec_serial_solve",
     "hec_prep_destroy", "hec_bp_build", "hec_bp_dims", "hec_bp_maps", "hec_bp_prepared", "hec_bp_apply_host",
