@@ -18,7 +18,7 @@ HOST_FLAGS := -O3 -std=c++20 -fPIC -fopenmp -ffp-contract=off -Wall -Wextra -Iin
 CU_FLAGS   := -O3 -std=c++20 $(ARCH) -lineinfo -fmad=false -Xptxas -v \
               -Xcompiler -fPIC,-fopenmp,-ffp-contract=off -Iinclude
 
-HOST_SRCS := $(wildcard $(SRC)/host/*.cpp) $(SRC)/cuda/tri_plan.cpp
+HOST_SRCS := $(wildcard $(SRC)/host/*.cpp) $(wildcard $(SRC)/cuda/*.cpp)
 CAPI_SRCS := $(wildcard $(SRC)/capi/*.cpp)
 CU_SRCS   := $(wildcard $(SRC)/cuda/*.cu)
 
@@ -34,7 +34,7 @@ all: lib oracle
 lib: $(LIB)
 
 $(LIB): $(HOST_OBJS) $(CAPI_OBJS) $(CU_OBJS)
-	$(NVCC) -shared $(ARCH) -cudart static -Xcompiler -fopenmp -o $@ $^ -lgomp
+	$(NVCC) -shared $(ARCH) -cudart static -Xcompiler -fopenmp -o $@ $^ -lgomp -ldl
 
 $(OBJ)/%.o: $(SRC)/%.cpp $(HEADERS)
 	@mkdir -p $(dir $@)

@@ -415,36 +415,47 @@ def ras_reference(size, blocks, restart=30):
 
 
 def ras_gmres(H, torch, rank, world, device, size, restart=30):
-    """RAS-ILU(0) GMRES(restart) time-to-solution, one subdomain per GPU
-    (BASELINE config 4). Max over ranks."""
+    """RAS-ILU(0) GMRES(restart) time-to-solution, one subdomain per GPU (BASELINE
+    config 4), through the library's C++ RAS layer (hec_ras_create / hec_ras_gmres_device:
+    NCCL halo exchanges and all-reduces under torchrun). Device-resident b and x,
+    CUDA events on the solve's stream, max over ranks."""
     from paper_1606_00541_b200 import ras
     t0 = time.time()
     a = H.gen_poisson7(size, size, size)
-    b = H.spmv_csr(a, np.ones(a.n_rows), workers=os.cpu_count())
-    solver = ras.RasGmres(a, overlap=1, restart=restart, device=device)
+    b = H.spmv_csr(a, np.ones(a.n_rows))
+    solver = ras.RasSolver(a, overlap=1)
+    plan = solver.plan
     setup = time.time() - t0
-    log(f"[bench] RAS setup {setup:.1f}s; warm-up solve")
-    solver.solve(b)  # warm-up: device layouts, workspaces, NCCL channels
+    log(f"[bench] RAS {size}^3 x{world}: setup {setup:.1f}s ({solver.comm}); warm-up solve")
+    bd = torch.tensor(b[plan.own], dtype=torch.float64, device=device)
+    xd = torch.empty_like(bd)
+    stream = torch.cuda.current_stream(device)
+    solver.gmres_device(bd, xd, restart=restart, stream=stream)  # warm-up: layouts, workspaces, NCCL channels
     torch.cuda.synchronize(device)
     if world > 1:
         torch.distributed.barrier()
-    t1 = time.perf_counter()
-    x, rep = solver.solve(b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = solver.gmres_device(bd, xd, restart=restart, stream=stream)
+    e1.record(stream)
     torch.cuda.synchronize(device)
-    sec = time.perf_counter() - t1
-    err = float((x - 1.0).abs().max().item())
+    sec = e0.elapsed_time(e1) * 1e-3
+    err = float((xd - 1.0).abs().max().item())
     if world > 1:
         t = torch.tensor([sec, err], dtype=torch.float64, device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         sec, err = float(t[0].item()), float(t[1].item())
-    log(f"[bench] RAS {size}^3 x{world}: {rep.iterations} iterations in {sec*1e3:.1f} ms (setup {setup:.1f}s)")
+    log(f"[bench] RAS {size}^3 x{world}: {rep.iterations} iterations in {sec*1e3:.1f} ms")
     return {"workload": f"RAS-ILU(0) GMRES({restart}), 7-pt Poisson {size}^3, overlap 1, {world} block(s) = GPU(s), "
                         f"b = A*1, rel_tol 1e-6",
             "seconds": round(sec, 5), "iterations": rep.iterations, "converged": rep.converged,
-            "final_relative_residual": rep.final_relative_residual, "ms_per_iteration": round(1e3 * sec / max(rep.iterations, 1), 4),
+            "final_relative_residual": rep.final_relative_residual,
+            "ms_per_iteration": round(1e3 * sec / max(rep.iterations, 1), 4),
             "max_abs_error_vs_ones": err, "allreduces": rep.allreduces, "halo_exchanges": rep.exchanges,
-            "rows_per_gpu": solver.plan.n_own, "halo_rows": int(len(solver.plan.halo)),
-            "collectives": "NCCL all_reduce (dots) + all_to_all_single (halo)" if world > 1 else "none"}
+            "gpu_launches": rep.launches, "rows_per_gpu": plan.n_own, "halo_rows": int(len(plan.halo)),
+            "setup_seconds": round(setup, 1),
+            "collectives": ("NCCL all-reduce (2 per iteration, CGS2) + grouped ncclSend/ncclRecv halo exchange"
+                            if solver.comm == "nccl" else solver.comm)}
 
 
 def main():

@@ -339,6 +339,80 @@ int hec_gmres_host(hec_csr_t a, const double* b, hec_bp_t m, const hec_gmres_con
                    double* x, hec_gmres_report* report, double* inner_residuals,
                    int inner_capacity);
 
+/* ===================== Section 3: multi-GPU RAS ======================== */
+/*
+ * Restricted Additive Schwarz with one subdomain per process / GPU
+ * (reference proj/src/precond.cpp:74-145 build_preconditioner(ras) + apply,
+ * proj/src/partition.cpp:28-107, proj/src/gmres.cpp:28-137 with the
+ * preconditioner). Rank g of `world` owns part g of partition_graph(A, world)
+ * and keeps local vectors [own | halo]; its block is extract_block(A, ext_g)
+ * factored with ILU(0) / ILUT / ILU(k) and solved by this library's kernels.
+ * Every call marked "collective" must be made by all ranks.
+ */
+typedef struct hec_ras_plan* hec_ras_plan_t;
+/* Host plan of one rank (no device, no communication; deterministic on every rank). */
+int hec_ras_plan_create(hec_csr_t a, int world, int rank, int overlap, hec_ras_plan_t* out);
+/* Borrowed views, valid until the plan (or the hec_ras_t owning it) is destroyed:
+ * own[n_own] and ext[n_ext] ascending global rows, halo[n_halo] by (owner, row),
+ * send_offsets / recv_offsets [world + 1] (peer p's segments), send_idx[n_send]
+ * (own positions sent, in the peer's halo order), gather / out_index [n_ext]
+ * (block row -> local [own | halo] index; -> own position or -1). */
+typedef struct {
+    int n, rank, world, overlap, n_own, n_halo, n_ext, n_send;
+    const int* own;
+    const int* halo;
+    const int* ext;
+    const int* send_offsets;
+    const int* send_idx;
+    const int* recv_offsets;
+    const int* gather;
+    const int* out_index;
+    const int* part_of; /* [n] */
+} hec_ras_plan_view;
+int hec_ras_plan_view_get(hec_ras_plan_t p, hec_ras_plan_view* v);
+int hec_ras_plan_destroy(hec_ras_plan_t p);
+
+/* Communication between the ranks. */
+enum { HEC_COMM_NONE = 0, HEC_COMM_NCCL = 1, HEC_COMM_CALLBACKS = 2 };
+typedef struct {
+    void* ctx;
+    /* in place sum over ranks of count doubles (host buffer); return 0 on success */
+    int (*allreduce_sum)(void* ctx, double* buf, int count);
+    /* halo exchange: send[send_offsets[p] ..) goes to peer p, recv[recv_offsets[p] ..)
+     * comes from p (offsets of the rank's plan); return 0 on success */
+    int (*exchange)(void* ctx, const double* send, int send_count, double* recv, int recv_count);
+} hec_comm_callbacks;
+typedef struct {
+    int kind;                      /* HEC_COMM_*                                        */
+    int rank, world;
+    const unsigned char* nccl_id;  /* HEC_COMM_NCCL: 128 bytes from hec_nccl_unique_id   */
+    hec_comm_callbacks callbacks;  /* HEC_COMM_CALLBACKS                                 */
+} hec_comm_spec;
+/* NCCL (opened at first use; a process that already loaded libnccl shares it). */
+int hec_nccl_unique_id(unsigned char id[128]);
+int hec_nccl_version(void); /* 0 if libnccl cannot be opened */
+
+typedef struct hec_ras* hec_ras_t;
+/* Collective. local_kind: 0 ilu0 (ras / bilu0), 1 ilut(ilut_p, ilut_tol), 3 ilu_k(fill_level).
+ * The communicator spans `comm->world` ranks (HEC_COMM_NONE: world 1). */
+int hec_ras_create(hec_csr_t a, int overlap, int local_kind, int ilut_p, double ilut_tol, int fill_level,
+                   const hec_comm_spec* comm, hec_ras_t* out);
+int hec_ras_get_plan(hec_ras_t r, hec_ras_plan_t* plan); /* borrowed */
+/* Collective: z_own = M^-1 r_own (halo exchange, local L and U solves, restricted
+ * scatter): rank g's rows of the reference's apply(ras, world blocks), bitwise. */
+int hec_ras_apply(hec_ras_t r, const double* r_own_dev, double* z_own_dev, void* stream);
+int hec_ras_apply_host(hec_ras_t r, const double* r_own, double* z_own);
+/* Collective: RAS-preconditioned GMRES(m) on the owned rows (host vectors, n_own).
+ * Two all-reduces and two halo exchanges per iteration (CGS2). */
+int hec_ras_gmres(hec_ras_t r, const double* b_own, const hec_gmres_config* cfg, double* x_own,
+                  hec_gmres_report* report, double* inner_residuals, int inner_capacity);
+/* Same with device vectors, enqueued on `stream` (returns when done). */
+int hec_ras_gmres_device(hec_ras_t r, const double* b_own_dev, const hec_gmres_config* cfg, double* x_own_dev,
+                         hec_gmres_report* report, double* inner_residuals, int inner_capacity, void* stream);
+/* counters of the last hec_ras_gmres*: all-reduces, halo exchanges, our kernel launches */
+int hec_ras_stats(hec_ras_t r, long long* allreduces, long long* exchanges, long long* launches);
+int hec_ras_destroy(hec_ras_t r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,27 @@ class PrepView(C.Structure):
                 ("csr_nnz", c_ll)]
 
 
+class RasPlanView(C.Structure):
+    _fields_ = [("n", c_int), ("rank", c_int), ("world", c_int), ("overlap", c_int), ("n_own", c_int),
+                ("n_halo", c_int), ("n_ext", c_int), ("n_send", c_int), ("own", P_int), ("halo", P_int),
+                ("ext", P_int), ("send_offsets", P_int), ("send_idx", P_int), ("recv_offsets", P_int),
+                ("gather", P_int), ("out_index", P_int), ("part_of", P_int)]
+
+
+COMM_NONE, COMM_NCCL, COMM_CALLBACKS = 0, 1, 2
+ALLREDUCE_CB = C.CFUNCTYPE(c_int, c_void_p, P_dbl, c_int)
+EXCHANGE_CB = C.CFUNCTYPE(c_int, c_void_p, P_dbl, c_int, P_dbl, c_int)
+
+
+class CommCallbacks(C.Structure):
+    _fields_ = [("ctx", c_void_p), ("allreduce_sum", ALLREDUCE_CB), ("exchange", EXCHANGE_CB)]
+
+
+class CommSpec(C.Structure):
+    _fields_ = [("kind", c_int), ("rank", c_int), ("world", c_int), ("nccl_id", C.POINTER(C.c_ubyte)),
+                ("callbacks", CommCallbacks)]
+
+
 def _sig(name, restype, *argtypes):
     f = getattr(lib, name)
     f.restype = restype
@@ -153,6 +174,21 @@ _sig("hec_bp_prepared", c_int, c_void_p, C.POINTER(c_void_p), C.POINTER(c_void_p
 _sig("hec_bp_apply_host", c_int, c_void_p, P_dbl, P_dbl)
 _sig("hec_bp_device", c_int, c_void_p, C.POINTER(c_void_p))
 _sig("hec_bp_destroy", c_int, c_void_p)
+# multi-GPU RAS
+_sig("hec_ras_plan_create", c_int, c_void_p, c_int, c_int, c_int, C.POINTER(c_void_p))
+_sig("hec_ras_plan_view_get", c_int, c_void_p, C.POINTER(RasPlanView))
+_sig("hec_ras_plan_destroy", c_int, c_void_p)
+_sig("hec_nccl_unique_id", c_int, C.POINTER(C.c_ubyte))
+_sig("hec_nccl_version", c_int)
+_sig("hec_ras_create", c_int, c_void_p, c_int, c_int, c_int, c_dbl, c_int, C.POINTER(CommSpec), C.POINTER(c_void_p))
+_sig("hec_ras_get_plan", c_int, c_void_p, C.POINTER(c_void_p))
+_sig("hec_ras_apply", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_ras_apply_host", c_int, c_void_p, P_dbl, P_dbl)
+_sig("hec_ras_gmres", c_int, c_void_p, P_dbl, C.POINTER(GmresConfig), P_dbl, C.POINTER(GmresReport), P_dbl, c_int)
+_sig("hec_ras_gmres_device", c_int, c_void_p, c_void_p, C.POINTER(GmresConfig), c_void_p, C.POINTER(GmresReport),
+     P_dbl, c_int, c_void_p)
+_sig("hec_ras_stats", c_int, c_void_p, C.POINTER(c_ll), C.POINTER(c_ll), C.POINTER(c_ll))
+_sig("hec_ras_destroy", c_int, c_void_p)
 _sig("hec_gmres_host", c_int, c_void_p, P_dbl, c_void_p, C.POINTER(GmresConfig), P_dbl,
      C.POINTER(GmresReport), P_dbl, c_int)
 
@@ -172,6 +208,9 @@ EXPORTED = [
     "hec_prepare", "hec_prep_view_get", "hec_prep_solve_host", "hec_prep_device", "hec_serial_solve",
     "hec_prep_destroy", "hec_bp_build", "hec_bp_dims", "hec_bp_maps", "hec_bp_prepared", "hec_bp_apply_host",
     "hec_bp_device", "hec_bp_destroy", "hec_gmres_host",
+    "hec_ras_plan_create", "hec_ras_plan_view_get", "hec_ras_plan_destroy", "hec_nccl_unique_id", "hec_nccl_version",
+    "hec_ras_create", "hec_ras_get_plan", "hec_ras_apply", "hec_ras_apply_host", "hec_ras_gmres",
+    "hec_ras_gmres_device", "hec_ras_stats", "hec_ras_destroy",
 ]
 
 

@@ -14,8 +14,10 @@
 #include <string>
 #include <vector>
 
+#include "../cuda/comm.hpp"
 #include "../cuda/device_runtime.hpp"
 #include "../cuda/krylov.hpp"
+#include "../host/ras_plan.hpp"
 #include "hecsolve/device.hpp"
 #include "hecsolve/errors.hpp"
 #include "hecsolve/gmres.hpp"
@@ -49,6 +51,22 @@ struct hec_krylov {
 };
 struct hec_hec {
     hec::HecMatrix m;
+};
+struct hec_ras_plan {
+    hec::ras::Plan plan;
+};
+struct hec_ras {
+    hec_ras_plan p;
+    std::unique_ptr<hec::dev::Comm> comm;
+    std::unique_ptr<hec::dev::DevicePrecond> M;
+    std::unique_ptr<hec::dev::DeviceSpmv> A;
+    hec::dev::DevBuf<int> send_idx;
+    hec::dev::DevBuf<double> vloc, sendbuf, h_r, h_z;
+    cudaStream_t stream = nullptr;
+    long long allreduces = 0, exchanges = 0, launches = 0;
+    ~hec_ras() {
+        if (stream) cudaStreamDestroy(stream);
+    }
 };
 struct hec_partition {
     int n = 0, parts = 0;
@@ -941,6 +959,202 @@ int hec_gmres_host(hec_csr_t a, const double* b, hec_bp_t m, const hec_gmres_con
         o.inner_residuals = res.report.inner_residuals;
         fill_report(o, report, inner_residuals, inner_capacity);
     });
+}
+
+// ---- multi-GPU RAS ----
+int hec_ras_plan_create(hec_csr_t a, int world, int rank, int overlap, hec_ras_plan_t* out) {
+    return guarded([&] {
+        need(a, "hec_ras_plan_create");
+        need(out, "hec_ras_plan_create");
+        auto h = std::make_unique<hec_ras_plan>();
+        h->plan = hec::ras::make_plan(a->m, world, rank, overlap);
+        *out = h.release();
+    });
+}
+
+int hec_ras_plan_view_get(hec_ras_plan_t p, hec_ras_plan_view* v) {
+    return guarded([&] {
+        need(p, "hec_ras_plan_view_get");
+        need(v, "hec_ras_plan_view_get");
+        const hec::ras::Plan& P = p->plan;
+        v->n = P.n;
+        v->rank = P.rank;
+        v->world = P.world;
+        v->overlap = P.overlap;
+        v->n_own = P.n_own();
+        v->n_halo = static_cast<int>(P.halo.size());
+        v->n_ext = static_cast<int>(P.ext.size());
+        v->n_send = static_cast<int>(P.send_idx.size());
+        v->own = P.own.data();
+        v->halo = P.halo.data();
+        v->ext = P.ext.data();
+        v->send_offsets = P.send_offsets.data();
+        v->send_idx = P.send_idx.data();
+        v->recv_offsets = P.recv_offsets.data();
+        v->gather = P.gather.data();
+        v->out_index = P.out_index.data();
+        v->part_of = P.part_of.data();
+    });
+}
+
+int hec_ras_plan_destroy(hec_ras_plan_t p) {
+    return guarded([&] { delete p; });
+}
+
+int hec_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        need(id, "hec_nccl_unique_id");
+        hec::dev::nccl_unique_id(id);
+    });
+}
+
+int hec_nccl_version(void) { return hec::dev::nccl_version(); }
+
+int hec_ras_create(hec_csr_t a, int overlap, int local_kind, int ilut_p, double ilut_tol, int fill_level,
+                   const hec_comm_spec* comm, hec_ras_t* out) {
+    return guarded([&] {
+        need(a, "hec_ras_create");
+        need(out, "hec_ras_create");
+        hec::dev::require_device();
+        const int kind = comm ? comm->kind : HEC_COMM_NONE;
+        const int world = kind == HEC_COMM_NONE ? 1 : comm->world;
+        const int rank = kind == HEC_COMM_NONE ? 0 : comm->rank;
+        auto h = std::make_unique<hec_ras>();
+        h->p.plan = hec::ras::make_plan(a->m, world, rank, overlap);
+        const hec::ras::Plan& P = h->p.plan;
+        // the rank's block: the reference's per-part factorisation (precond.cpp:97-110)
+        const hec::CsrMatrix blk = hec::extract_block(a->m, P.ext);
+        hec::IluFactors f;
+        try {
+            f = local_kind == 1   ? hec::ilut(blk, ilut_p, ilut_tol)
+                : local_kind == 3 ? hec::ilu_k(blk, fill_level)
+                                  : hec::ilu0(blk);
+        } catch (const hec::ZeroPivotError& e) {
+            throw hec::ZeroPivotError(e.row(), rank);  // re-tagged with the block (precond.cpp:107-109)
+        }
+        const hec::PreparedTriangular pl = hec::prepare_lower(f.l), pu = hec::prepare_upper(f.u);
+        h->M = std::make_unique<hec::dev::DevicePrecond>(P.n_loc(), P.n_own(), static_cast<int>(P.ext.size()),
+                                                         P.gather.data(), P.out_index.data(), hec::source_of(pl),
+                                                         hec::source_of(pu), hec::tri_options(nullptr));
+        h->A = std::make_unique<hec::dev::DeviceSpmv>(P.a_local.n_rows, P.a_local.n_cols,
+                                                      P.a_local.row_offsets.data(), P.a_local.col_indices.data(),
+                                                      P.a_local.values.data());
+        h->send_idx.upload(P.send_idx);
+        if (kind == HEC_COMM_NCCL) {
+            need(comm->nccl_id, "hec_ras_create (nccl_id)");
+            h->comm = std::make_unique<hec::dev::NcclComm>(comm->nccl_id, rank, world);
+        } else if (kind == HEC_COMM_CALLBACKS) {
+            if (!comm->callbacks.allreduce_sum || !comm->callbacks.exchange)
+                throw std::invalid_argument("hec_ras_create: missing callbacks");
+            hec::dev::CommCallbacks cb;
+            cb.ctx = comm->callbacks.ctx;
+            cb.allreduce_sum = comm->callbacks.allreduce_sum;
+            cb.exchange = comm->callbacks.exchange;
+            h->comm = std::make_unique<hec::dev::CallbackComm>(cb, rank, world);
+        } else if (kind == HEC_COMM_NONE) {
+            h->comm = std::make_unique<hec::dev::NullComm>();
+        } else {
+            throw std::invalid_argument("hec_ras_create: unknown comm kind");
+        }
+        HEC_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        *out = h.release();
+    });
+}
+
+int hec_ras_get_plan(hec_ras_t r, hec_ras_plan_t* plan) {
+    return guarded([&] {
+        need(r, "hec_ras_get_plan");
+        need(plan, "hec_ras_get_plan");
+        *plan = &r->p;
+    });
+}
+
+namespace {
+hec::dev::DistSystem ras_system(hec_ras_t r) {
+    const hec::ras::Plan& P = r->p.plan;
+    hec::dev::DistSystem S;
+    S.n_own = P.n_own();
+    S.n_loc = P.n_loc();
+    S.A = r->A.get();
+    S.M = r->M.get();
+    S.send_idx = r->send_idx.p;
+    S.n_send = static_cast<int>(P.send_idx.size());
+    S.send_off = P.send_offsets;
+    S.recv_off = P.recv_offsets;
+    S.comm = r->comm.get();
+    return S;
+}
+}  // namespace
+
+int hec_ras_apply(hec_ras_t r, const double* r_own_dev, double* z_own_dev, void* stream) {
+    return guarded([&] {
+        need(r, "hec_ras_apply");
+        const hec::ras::Plan& P = r->p.plan;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (r->vloc.count < static_cast<std::size_t>(std::max(P.n_loc(), 1))) r->vloc.alloc(std::max(P.n_loc(), 1));
+        if (r->sendbuf.count < std::max<std::size_t>(P.send_idx.size(), 1)) r->sendbuf.alloc(std::max<std::size_t>(P.send_idx.size(), 1));
+        HEC_CUDA(cudaMemcpyAsync(r->vloc.p, r_own_dev, sizeof(double) * P.n_own(), cudaMemcpyDeviceToDevice, st));
+        hec::dev::halo_exchange(ras_system(r), r->vloc.p, r->sendbuf.p, st);
+        r->M->apply(r->vloc.p, z_own_dev, st);
+    });
+}
+
+int hec_ras_apply_host(hec_ras_t r, const double* r_own, double* z_own) {
+    return guarded([&] {
+        need(r, "hec_ras_apply_host");
+        const int n = r->p.plan.n_own();
+        if (r->h_r.count < static_cast<std::size_t>(std::max(n, 1))) {
+            r->h_r.alloc(std::max(n, 1));
+            r->h_z.alloc(std::max(n, 1));
+        }
+        HEC_CUDA(cudaMemcpyAsync(r->h_r.p, r_own, sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
+        if (hec_ras_apply(r, r->h_r.p, r->h_z.p, r->stream) != HEC_OK) throw std::runtime_error(t_msg);
+        HEC_CUDA(cudaMemcpyAsync(z_own, r->h_z.p, sizeof(double) * n, cudaMemcpyDeviceToHost, r->stream));
+        HEC_CUDA(cudaStreamSynchronize(r->stream));
+    });
+}
+
+int hec_ras_gmres_device(hec_ras_t r, const double* b_own_dev, const hec_gmres_config* cfg, double* x_own_dev,
+                         hec_gmres_report* report, double* inner_residuals, int inner_capacity, void* stream) {
+    return guarded([&] {
+        need(r, "hec_ras_gmres_device");
+        need(cfg, "hec_ras_gmres_device");
+        hec::dev::GmresParams gp{cfg->restart, cfg->max_iters, cfg->rel_tol, cfg->abs_tol};
+        hec::dev::DistSystem S = ras_system(r);
+        const long long a0 = r->comm->allreduces, e0 = r->comm->exchanges;
+        const auto o = hec::dev::gmres_dist(S, b_own_dev, x_own_dev, gp, static_cast<cudaStream_t>(stream));
+        r->allreduces = r->comm->allreduces - a0;
+        r->exchanges = r->comm->exchanges - e0;
+        r->launches = o.launches;
+        fill_report(o, report, inner_residuals, inner_capacity);
+    });
+}
+
+int hec_ras_gmres(hec_ras_t r, const double* b_own, const hec_gmres_config* cfg, double* x_own,
+                  hec_gmres_report* report, double* inner_residuals, int inner_capacity) {
+    return guarded([&] {
+        need(r, "hec_ras_gmres");
+        const int n = r->p.plan.n_own();
+        hec::dev::DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+        HEC_CUDA(cudaMemcpyAsync(b.p, b_own, sizeof(double) * n, cudaMemcpyHostToDevice, r->stream));
+        const int rc = hec_ras_gmres_device(r, b.p, cfg, x.p, report, inner_residuals, inner_capacity, r->stream);
+        if (rc != HEC_OK) throw std::runtime_error(t_msg);
+        HEC_CUDA(cudaMemcpyAsync(x_own, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, r->stream));
+        HEC_CUDA(cudaStreamSynchronize(r->stream));
+    });
+}
+
+int hec_ras_stats(hec_ras_t r, long long* allreduces, long long* exchanges, long long* launches) {
+    return guarded([&] {
+        need(r, "hec_ras_stats");
+        if (allreduces) *allreduces = r->allreduces;
+        if (exchanges) *exchanges = r->exchanges;
+        if (launches) *launches = r->launches;
+    });
+}
+
+int hec_ras_destroy(hec_ras_t r) {
+    return guarded([&] { delete r; });
 }
 
 }  // extern "C"

@@ -392,6 +392,17 @@ void DevicePrecond::compose() {
     lu_map_.upload(m);
 }
 
+cudaStream_t DevicePrecond::host_stream(std::unique_lock<std::mutex>& lock) {
+    lock = std::unique_lock<std::mutex>(h_mu_);
+    if (!h_stream_) HEC_CUDA(cudaStreamCreateWithFlags(&h_stream_, cudaStreamNonBlocking));
+    return h_stream_;
+}
+
+int DevicePrecond::launches_per_apply() const {
+    if (n_ext_ == 0) return 0;
+    return l_->launches_per_solve() + u_->launches_per_solve() - (identity_ ? 1 : 2);
+}
+
 void DevicePrecond::apply_host(const double* r, double* x) {
     if (n_ == 0 && n_out_ == 0) return;
     std::lock_guard<std::mutex> g(h_mu_);

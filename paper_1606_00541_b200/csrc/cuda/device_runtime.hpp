@@ -153,6 +153,10 @@ public:
                   plan::TriSource u, const TriOptions& opt);
     void apply(const double* r, double* x, cudaStream_t st);
     void apply_host(const double* r, double* x);
+    // The handle's own stream (created on first use) with the lock that
+    // serialises host-path users of it; workspaces stay bound to this stream.
+    cudaStream_t host_stream(std::unique_lock<std::mutex>& lock);
+    int launches_per_apply() const;
     const DeviceTri& lower() const { return *l_; }
     const DeviceTri& upper() const { return *u_; }
     int n() const { return n_; }

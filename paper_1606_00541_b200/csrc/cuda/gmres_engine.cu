@@ -1,0 +1,415 @@
+// Restarted right-preconditioned GMRES(m) on one GPU or on several (RAS: one
+// subdomain per rank), zero initial guess.
+//
+// Control flow, tolerances, the lucky-breakdown / stall logic, the Givens
+// rotations, the back substitution and every reported quantity follow the
+// reference proj/src/gmres.cpp:28-137 line for line (host arithmetic, same
+// order). The n-length work runs on the GPU:
+//
+//   w = A M^-1 v_j      halo exchange of v_j (RAS), local ILU apply (the
+//                       persistent k_wave triangular solves), halo exchange of
+//                       z, HEC SpMV of the owned rows
+//   orthogonalisation   classical Gram-Schmidt with one re-orthogonalisation
+//                       (CGS2) instead of the reference's modified Gram-Schmidt
+//                       (gmres.cpp:72-77): the j+1 dots of a pass are one fused
+//                       multi-vector kernel and ONE all-reduce, so an iteration
+//                       costs two all-reduces (pass 1: V^T w; pass 2: V^T w' and
+//                       ||w'||^2) instead of j+2. h = h1 + h2 and
+//                       ||w''||^2 = ||w'||^2 - ||h2||^2 (V orthonormal).
+//                       In exact arithmetic CGS2 and MGS produce the same
+//                       Hessenberg matrix; rounding differs, so iteration counts
+//                       are compared within +-1.
+//   restart             x += M^-1 (V y), r = b - A x (fused residual SpMV).
+//
+// Dots are deterministic: per-thread sums in a fixed element order, fixed
+// block trees, and a fixed-order final sum by the last block (then the
+// all-reduce across ranks).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "comm.hpp"
+#include "device_runtime.hpp"
+#include "gmres_engine.hpp"
+
+namespace hec::dev {
+
+namespace {
+
+constexpr int kT = 256;       // threads per block
+constexpr int kKG = 32;       // basis vectors per fused pass
+constexpr int kMaxOut = kKG + 1;
+
+// Block-reduces acc[0..kc) and, with_norm, acc[kKG] (as output kc) to
+// partials[k * grid + block]; the last block to finish sums partials[k * grid +
+// 0..grid) in a fixed order into out[k]. Fixed shapes: run-to-run reproducible.
+__device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int with_norm, double* partials,
+                                           unsigned* counter, double* out) {
+    __shared__ double sw[kMaxOut][kT / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cnt = kc + (with_norm ? 1 : 0);
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) {
+        const bool use = k < kc || (k == kKG && with_norm);
+        if (use) {
+            double v = acc[k];
+            for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+            if (lane == 0) sw[k < kc ? k : kc][warp] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kT / 32; ++q) s = __dadd_rn(s, sw[threadIdx.x][q]);
+        partials[static_cast<size_t>(threadIdx.x) * gridDim.x + blockIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int k = warp; k < cnt; k += kT / 32) {  // one warp per output, fixed order
+        double s = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32)
+            s = __dadd_rn(s, __ldcg(&partials[static_cast<size_t>(k) * gridDim.x + b]));
+        for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+        if (lane == 0) out[k] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0;
+}
+
+// out[k] = V_k . w for k < kc (kc <= kKG); with_norm: out[kc] = w . w.
+__global__ void __launch_bounds__(kT) k_mdot(int n, const double* __restrict__ V, size_t ldv, int kc,
+                                             const double* __restrict__ w, int with_norm, double* partials,
+                                             unsigned* counter, double* out) {
+    double acc[kMaxOut];
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
+    const int stride = gridDim.x * kT;
+    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+        const double wi = w[i];
+#pragma unroll
+        for (int k = 0; k < kKG; ++k)
+            if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(__ldg(V + k * ldv + i), wi));
+        acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(wi, wi));
+    }
+    reduce_out(acc, kc, with_norm, partials, counter, out);
+}
+
+// w_out = (w_in - sum_{k<kc} c_k V_k) / s  (k in order; s = 1 unless scaled), where
+//   scale_mode 0: no scaling
+//   scale_mode 1: s = scale_val
+//   scale_mode 2: s = sqrt(max(0, c[kc] - sum_k c_k^2)) (the CGS2 norm), written to *s_out
+// with_dots: out[k] = V_k . w_out (k < kc), out[kc] = w_out . w_out.
+__global__ void __launch_bounds__(kT) k_mupdate(int n, const double* __restrict__ V, size_t ldv, int kc,
+                                                const double* __restrict__ c, const double* w_in, double* w_out,
+                                                int scale_mode, double scale_val, double* s_out, int with_dots,
+                                                double* partials, unsigned* counter, double* out) {
+    __shared__ double sc[kMaxOut];
+    __shared__ double s_scale;
+    if (threadIdx.x < kc) sc[threadIdx.x] = c[threadIdx.x];
+    if (threadIdx.x == 0) {
+        double s = 1.0;
+        if (scale_mode == 1) s = scale_val;
+        if (scale_mode == 2) {
+            double h2 = 0.0;
+            for (int k = 0; k < kc; ++k) h2 = __dadd_rn(h2, __dmul_rn(c[k], c[k]));
+            s = __dsqrt_rn(fmax(__dsub_rn(c[kc], h2), 0.0));
+            if (blockIdx.x == 0) *s_out = s;
+            if (!(s > 0.0)) s = 1.0;  // breakdown: the column is never used (gmres.cpp:79-83)
+        }
+        s_scale = s;
+    }
+    __syncthreads();
+    const double s = s_scale;
+    double acc[kMaxOut];
+#pragma unroll
+    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
+    const int stride = gridDim.x * kT;
+    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+        double vk[kKG];
+        double wi = w_in[i];
+#pragma unroll
+        for (int k = 0; k < kKG; ++k)
+            if (k < kc) {
+                vk[k] = __ldg(V + k * ldv + i);
+                wi = __dsub_rn(wi, __dmul_rn(sc[k], vk[k]));
+            }
+        if (scale_mode) wi = __ddiv_rn(wi, s);
+        w_out[i] = wi;
+        if (with_dots) {
+#pragma unroll
+            for (int k = 0; k < kKG; ++k)
+                if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(vk[k], wi));
+            acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(wi, wi));
+        }
+    }
+    if (!with_dots) return;
+    reduce_out(acc, kc, 1, partials, counter, out);
+}
+
+// xc = sum_{i<j} y_i V_i, accumulated in i order from 0.0 (gmres.cpp:121-122)
+__global__ void k_combine_v(int n, int j, double* xc, const double* V, size_t ldv, const double* y) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < j; ++i) s = __dadd_rn(s, __dmul_rn(y[i], V[i * ldv + t]));
+        xc[t] = s;
+    }
+}
+
+__global__ void k_add_v(int n, double* x, const double* d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        x[i] = __dadd_rn(x[i], d[i]);
+}
+
+// send[i] = v[idx[i]] (halo pack)
+__global__ void k_pack(int m, const int* __restrict__ idx, const double* v, double* send) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) send[i] = v[idx[i]];
+}
+
+int sm_count() {
+    int dev = 0, sms = 0;
+    HEC_CUDA(cudaGetDevice(&dev));
+    HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+
+}  // namespace
+
+void halo_exchange(const DistSystem& S, double* vloc, double* sendbuf, cudaStream_t st) {
+    if (!S.comm || S.comm->world() == 1) return;
+    if (S.n_send) {
+        const int vb = 256;
+        k_pack<<<std::max(1, std::min(4 * sm_count(), (S.n_send + vb - 1) / vb)), vb, 0, st>>>(S.n_send, S.send_idx,
+                                                                                             vloc, sendbuf);
+        HEC_CUDA(cudaGetLastError());
+    }
+    S.comm->exchange(sendbuf, S.send_off, vloc + S.n_own, S.recv_off, st);
+}
+
+GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const GmresParams& cfg,
+                        cudaStream_t st) {
+    if (cfg.restart < 1) throw std::invalid_argument("gmres: restart must be >= 1");
+    if (cfg.max_iters < 0) throw std::invalid_argument("gmres: max_iters must be >= 0");
+    if (cfg.rel_tol < 0.0 || cfg.abs_tol < 0.0) throw std::invalid_argument("gmres: tolerances must be >= 0");
+    if (!S.A || S.A->n_rows() != S.n_own || S.A->n_cols() != S.n_loc)
+        throw std::invalid_argument("gmres: operator size mismatch");
+    if (S.M && (S.M->n() != S.n_loc || S.M->n_out() != S.n_own))
+        throw std::invalid_argument("gmres: preconditioner size mismatch");
+    NullComm none;
+    Comm& comm = S.comm ? *S.comm : none;
+
+    const auto t0 = std::chrono::steady_clock::now();
+    const int n = S.n_own;
+    const int mr = cfg.restart;
+    GmresOutcome out;
+    const int grid = std::max(1, std::min(4 * sm_count(), (n + kT - 1) / kT));
+    const size_t ldv = static_cast<size_t>((std::max(S.n_loc, 1) + 31) / 32 * 32);  // 256-byte aligned columns
+
+    DevBuf<double> V(static_cast<size_t>(mr + 1) * ldv), w(ldv), zloc(ldv), xloc(ldv), xc(ldv), r(ldv), b(ldv);
+    DevBuf<double> hb(2 * static_cast<size_t>(mr) + 8), yv(static_cast<size_t>(mr) + 1);
+    DevBuf<double> partials(static_cast<size_t>(kMaxOut) * grid), sendbuf(std::max(S.n_send, 1));
+    DevBuf<unsigned> counter(1);
+    HEC_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), st));
+    HEC_CUDA(cudaMemsetAsync(xloc.p, 0, sizeof(double) * ldv, st));
+    HEC_CUDA(cudaMemcpyAsync(b.p, b_own, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    double* hb1 = hb.p;            // pass-1 dots (j+1)
+    double* hb2 = hb.p + mr + 2;   // pass-2 dots (j+1), ||w'||^2, ||w''||
+    std::vector<double> hh(2 * static_cast<size_t>(mr) + 8);
+
+    auto halo = [&](double* vloc) {  // fill vloc[n_own ..) from the owners
+        if (comm.world() == 1) return;
+        out.launches += S.n_send ? 1 : 0;
+        halo_exchange(S, vloc, sendbuf.p, st);
+    };
+    auto apply_op = [&](double* vloc, double* dst) {  // dst = A M^-1 v (own rows)
+        halo(vloc);
+        if (S.M) {
+            S.M->apply(vloc, zloc.p, st);
+            out.launches += S.M->launches_per_apply();
+            halo(zloc.p);
+            S.A->run(zloc.p, dst, st);
+        } else {
+            S.A->run(vloc, dst, st);
+        }
+        ++out.launches;
+    };
+    auto norm = [&](const double* v) {  // sqrt(sum over ranks of v . v)
+        k_mdot<<<grid, kT, 0, st>>>(n, nullptr, ldv, 0, v, 1, partials.p, counter.p, hb.p);
+        ++out.launches;
+        comm.allreduce_sum(hb.p, 1, st);
+        double s2 = 0.0;
+        HEC_CUDA(cudaMemcpyAsync(&s2, hb.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        HEC_CUDA(cudaStreamSynchronize(st));
+        return std::sqrt(s2);
+    };
+
+    const double bnorm = norm(b.p);
+    const double threshold = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
+    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr);
+    HEC_CUDA(cudaMemcpyAsync(r.p, b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    double rnorm = bnorm;
+    bool stalled = false;
+
+    while (true) {
+        if (rnorm <= threshold) {
+            out.converged = true;
+            break;
+        }
+        if (out.iterations >= cfg.max_iters || stalled) break;
+        // v_0 = r / rnorm (gmres.cpp:62)
+        k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, 0, hb.p, r.p, V.p, 1, rnorm, nullptr, 0, partials.p, counter.p,
+                                       nullptr);
+        ++out.launches;
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = rnorm;
+
+        int j = 0;
+        bool lucky = false;
+        while (j < mr && out.iterations < cfg.max_iters) {
+            double* vj = V.p + j * ldv;
+            apply_op(vj, w.p);
+            const int kc = j + 1;
+            if (kc <= kKG) {
+                // CGS2 pass 1: h1 = V^T w
+                k_mdot<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, w.p, 0, partials.p, counter.p, hb1);
+                comm.allreduce_sum(hb1, kc, st);
+                // pass 2: w' = w - V h1; h2 = V^T w', ||w'||^2
+                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, hb1, w.p, w.p, 0, 1.0, nullptr, 1, partials.p,
+                                               counter.p, hb2);
+                comm.allreduce_sum(hb2, kc + 1, st);
+                // v_{j+1} = (w' - V h2) / ||w''||
+                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0,
+                                               hb2 + kc + 1, 0, partials.p, counter.p, nullptr);
+                out.launches += 3;
+            } else {
+                // more basis vectors than one fused pass holds: modified Gram-Schmidt,
+                // one vector at a time (each step still one dot + one all-reduce)
+                for (int i = 0; i < kc; ++i) {
+                    k_mdot<<<grid, kT, 0, st>>>(n, V.p + i * ldv, ldv, 1, w.p, 0, partials.p, counter.p, hb1 + i);
+                    comm.allreduce_sum(hb1 + i, 1, st);
+                    k_mupdate<<<grid, kT, 0, st>>>(n, V.p + i * ldv, ldv, 1, hb1 + i, w.p, w.p, 0, 1.0, nullptr,
+                                                   i + 1 == kc, partials.p, counter.p, hb2 + kc - 1);
+                    out.launches += 2;
+                }
+                comm.allreduce_sum(hb2 + kc, 1, st);
+                HEC_CUDA(cudaMemsetAsync(hb2, 0, sizeof(double) * kc, st));
+                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, 0, hb2 + kc, w.p, V.p + (j + 1) * ldv, 2, 1.0,
+                                               hb2 + kc + 1, 0, partials.p, counter.p, nullptr);
+                ++out.launches;
+            }
+            HEC_CUDA(cudaMemcpyAsync(hh.data(), hb.p, sizeof(double) * (2 * mr + 8), cudaMemcpyDeviceToHost, st));
+            HEC_CUDA(cudaStreamSynchronize(st));
+            for (int i = 0; i <= j; ++i) h[i + j * (mr + 1)] = hh[i] + hh[mr + 2 + i];
+            const double hjj1 = hh[mr + 2 + kc + 1];
+            h[(j + 1) + j * (mr + 1)] = hjj1;
+            if (!(hjj1 > 1e-300)) lucky = true;
+
+            // Givens rotations (gmres.cpp:85-104)
+            for (int i = 0; i < j; ++i) {
+                const double hi = h[i + j * (mr + 1)];
+                const double hi1 = h[(i + 1) + j * (mr + 1)];
+                h[i + j * (mr + 1)] = cs[i] * hi + sn[i] * hi1;
+                h[(i + 1) + j * (mr + 1)] = -sn[i] * hi + cs[i] * hi1;
+            }
+            const double hjj = h[j + j * (mr + 1)];
+            const double denom = std::hypot(hjj, hjj1);
+            if (denom > 0.0) {
+                cs[j] = hjj / denom;
+                sn[j] = hjj1 / denom;
+            } else {
+                cs[j] = 1.0;
+                sn[j] = 0.0;
+            }
+            h[j + j * (mr + 1)] = denom;
+            h[(j + 1) + j * (mr + 1)] = 0.0;
+            const double gj = g[j];
+            g[j] = cs[j] * gj;
+            g[j + 1] = -sn[j] * gj;
+
+            ++out.iterations;
+            ++j;
+            const double est = std::fabs(g[j]);
+            out.inner_residuals.push_back(est);
+            if (est <= threshold || lucky) break;
+        }
+
+        // back substitution (gmres.cpp:113-119), x += M^-1 (V y), r = b - A x
+        for (int i = j - 1; i >= 0; --i) {
+            double s = g[i];
+            for (int t = i + 1; t < j; ++t) s -= h[i + t * (mr + 1)] * y[t];
+            y[i] = s / h[i + i * (mr + 1)];
+        }
+        HEC_CUDA(cudaMemcpyAsync(yv.p, y.data(), sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
+        k_combine_v<<<grid, kT, 0, st>>>(n, j, xc.p, V.p, ldv, yv.p);
+        ++out.launches;
+        if (S.M) {
+            halo(xc.p);
+            S.M->apply(xc.p, zloc.p, st);
+            out.launches += S.M->launches_per_apply();
+            k_add_v<<<grid, kT, 0, st>>>(n, xloc.p, zloc.p);
+        } else {
+            k_add_v<<<grid, kT, 0, st>>>(n, xloc.p, xc.p);
+        }
+        ++out.launches;
+        halo(xloc.p);
+        S.A->residual(b.p, xloc.p, r.p, st);
+        ++out.launches;
+        const double rn = norm(r.p);
+        if (lucky && rn > threshold) stalled = true;
+        rnorm = rn;
+    }
+    out.final_relative_residual = bnorm > 0.0 ? rnorm / bnorm : rnorm;
+    HEC_CUDA(cudaMemcpyAsync(x_own, xloc.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    HEC_CUDA(cudaStreamSynchronize(st));
+    HEC_CUDA(cudaGetLastError());
+    out.allreduces = comm.allreduces;
+    out.exchanges = comm.exchanges;
+    out.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return out;
+}
+
+// Single GPU: hec::gmres / hec_gmres_solve (one rank, no halo).
+GmresOutcome gmres_device(const DeviceSpmv& A, DevicePrecond* M, const double* b_host, const GmresParams& cfg,
+                          double* x_host) {
+    if (A.n_rows() != A.n_cols()) throw std::invalid_argument("gmres: matrix must be square");
+    if (M && M->n() != A.n_rows()) throw std::invalid_argument("gmres: preconditioner size mismatch");
+    const int n = A.n_rows();
+    DistSystem S;
+    S.n_own = S.n_loc = n;
+    S.A = &A;
+    S.M = M;
+    // one long-lived stream per preconditioner (its workspaces stay bound to it)
+    std::unique_lock<std::mutex> lock;
+    cudaStream_t st = nullptr;
+    cudaStream_t own = nullptr;
+    if (M) {
+        st = M->host_stream(lock);
+    } else {
+        HEC_CUDA(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+        st = own;
+    }
+    struct Guard {
+        cudaStream_t s;
+        ~Guard() {
+            if (s) cudaStreamDestroy(s);
+        }
+    } guard{own};
+    DevBuf<double> b(std::max(n, 1)), x(std::max(n, 1));
+    HEC_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    GmresOutcome o = gmres_dist(S, b.p, x.p, cfg, st);
+    HEC_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    HEC_CUDA(cudaStreamSynchronize(st));
+    o.solve_seconds = o.solve_seconds;  // measured inside gmres_dist (excludes the two copies)
+    return o;
+}
+
+}  // namespace hec::dev

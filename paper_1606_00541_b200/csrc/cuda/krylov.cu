@@ -176,164 +176,4 @@ void KrylovOps::sqrt(const double* in, double* out, cudaStream_t st) {
     HEC_CUDA(cudaGetLastError());
 }
 
-GmresOutcome gmres_device(const DeviceSpmv& A, DevicePrecond* M, const double* b_host, const GmresParams& cfg,
-                          double* x_host) {
-    if (A.n_rows() != A.n_cols()) throw std::invalid_argument("gmres: matrix must be square");
-    if (cfg.restart < 1) throw std::invalid_argument("gmres: restart must be >= 1");
-    if (cfg.max_iters < 0) throw std::invalid_argument("gmres: max_iters must be >= 0");
-    if (cfg.rel_tol < 0.0 || cfg.abs_tol < 0.0) throw std::invalid_argument("gmres: tolerances must be >= 0");
-    if (M && M->n() != A.n_rows()) throw std::invalid_argument("gmres: preconditioner size mismatch");
-
-    const auto t0 = std::chrono::steady_clock::now();
-    const int n = A.n_rows();
-    const int mr = cfg.restart;
-    GmresOutcome out;
-    cudaStream_t st = nullptr;
-    HEC_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct StreamGuard {
-        cudaStream_t s;
-        ~StreamGuard() { cudaStreamDestroy(s); }
-    } guard{st};
-
-    int dev = 0, sms = 0;
-    HEC_CUDA(cudaGetDevice(&dev));
-    HEC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int grid = std::max(1, std::min(4 * sms, (n + 2 * kThreads - 1) / (2 * kThreads)));
-    const size_t ldv = static_cast<size_t>((std::max(n, 1) + 3) / 4 * 4);  // 32-byte aligned basis columns
-
-    DevBuf<double> V((mr + 1) * ldv), w(ldv), z(ldv), r(ldv), x(ldv), b(ldv), yv(mr + 1);
-    DevBuf<double> hcol(mr + 3), partials(grid), scal(2);
-    DevBuf<unsigned> counter(1);
-    HEC_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), st));
-    HEC_CUDA(cudaMemcpyAsync(b.p, b_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    HEC_CUDA(cudaMemsetAsync(x.p, 0, sizeof(double) * ldv, st));
-    out.launches += 0;
-
-    auto dot_into = [&](const double* a, double* dst, double* dst_sqrt) {
-        // dot(a, a) via the fused kernel with no axpy part
-        k_mgs_step<<<grid, kThreads, 0, st>>>(n, const_cast<double*>(a), nullptr, nullptr, a, partials.p,
-                                                counter.p, dst, dst_sqrt);
-        ++out.launches;
-    };
-    auto fetch = [&](const double* src, double* dst, int count) {
-        HEC_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
-        HEC_CUDA(cudaStreamSynchronize(st));
-    };
-
-    double bn[2];
-    dot_into(b.p, scal.p, scal.p + 1);
-    fetch(scal.p, bn, 2);
-    const double bnorm = bn[1];
-    const double threshold = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
-
-    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr);
-    HEC_CUDA(cudaMemcpyAsync(r.p, b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    double rnorm = bnorm;
-    bool stalled = false;
-    double* rnorm_dev = scal.p + 1;  // holds ||r|| on the device
-
-    while (true) {
-        if (rnorm <= threshold) {
-            out.converged = true;
-            break;
-        }
-        if (out.iterations >= cfg.max_iters || stalled) break;
-        k_div<<<grid, kThreads, 0, st>>>(n, V.p, r.p, rnorm_dev);
-        ++out.launches;
-        std::fill(g.begin(), g.end(), 0.0);
-        g[0] = rnorm;
-
-        int j = 0;
-        bool lucky = false;
-        while (j < mr && out.iterations < cfg.max_iters) {
-            double* vj = V.p + j * ldv;
-            if (M) {
-                M->apply(vj, z.p, st);
-                out.launches += M->lower().launches_per_solve() + M->upper().launches_per_solve();
-                A.run(z.p, w.p, st);
-            } else {
-                A.run(vj, w.p, st);
-            }
-            ++out.launches;
-            // MGS: step i computes h_ij after removing the (i-1) component
-            for (int i = 0; i <= j; ++i) {
-                k_mgs_step<<<grid, kThreads, 0, st>>>(n, w.p, i ? V.p + (i - 1) * ldv : nullptr,
-                                                       i ? hcol.p + (i - 1) : nullptr, V.p + i * ldv,
-                                                       partials.p, counter.p, hcol.p + i, nullptr);
-                ++out.launches;
-            }
-            // last removal fused with ||w||^2, then v_{j+1} = w / ||w||
-            k_mgs_step<<<grid, kThreads, 0, st>>>(n, w.p, vj, hcol.p + j, w.p, partials.p, counter.p,
-                                                   hcol.p + j + 2, hcol.p + j + 1);
-            ++out.launches;
-            k_div<<<grid, kThreads, 0, st>>>(n, V.p + (j + 1) * ldv, w.p, hcol.p + j + 1);
-            ++out.launches;
-            std::vector<double> hc(j + 2);
-            fetch(hcol.p, hc.data(), j + 2);
-            for (int i = 0; i <= j; ++i) h[i + j * (mr + 1)] = hc[i];
-            const double hjj1 = hc[j + 1];
-            h[(j + 1) + j * (mr + 1)] = hjj1;
-            if (!(hjj1 > 1e-300)) lucky = true;
-
-            for (int i = 0; i < j; ++i) {
-                const double hi = h[i + j * (mr + 1)];
-                const double hi1 = h[(i + 1) + j * (mr + 1)];
-                h[i + j * (mr + 1)] = cs[i] * hi + sn[i] * hi1;
-                h[(i + 1) + j * (mr + 1)] = -sn[i] * hi + cs[i] * hi1;
-            }
-            const double hjj = h[j + j * (mr + 1)];
-            const double denom = std::hypot(hjj, hjj1);
-            if (denom > 0.0) {
-                cs[j] = hjj / denom;
-                sn[j] = hjj1 / denom;
-            } else {
-                cs[j] = 1.0;
-                sn[j] = 0.0;
-            }
-            h[j + j * (mr + 1)] = denom;
-            h[(j + 1) + j * (mr + 1)] = 0.0;
-            const double gj = g[j];
-            g[j] = cs[j] * gj;
-            g[j + 1] = -sn[j] * gj;
-
-            ++out.iterations;
-            ++j;
-            const double est = std::fabs(g[j]);
-            out.inner_residuals.push_back(est);
-            if (est <= threshold || lucky) break;
-        }
-
-        for (int i = j - 1; i >= 0; --i) {
-            double s = g[i];
-            for (int t = i + 1; t < j; ++t) s -= h[i + t * (mr + 1)] * y[t];
-            y[i] = s / h[i + i * (mr + 1)];
-        }
-        HEC_CUDA(cudaMemcpyAsync(yv.p, y.data(), sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
-        k_combine<<<grid, kThreads, 0, st>>>(n, j, w.p, V.p, ldv, yv.p);
-        ++out.launches;
-        if (M) {
-            M->apply(w.p, z.p, st);
-            out.launches += M->lower().launches_per_solve() + M->upper().launches_per_solve();
-            k_add<<<grid, kThreads, 0, st>>>(n, x.p, z.p);
-        } else {
-            k_add<<<grid, kThreads, 0, st>>>(n, x.p, w.p);
-        }
-        ++out.launches;
-        A.residual(b.p, x.p, r.p, st);
-        ++out.launches;
-        dot_into(r.p, scal.p, rnorm_dev);
-        double rr[2];
-        fetch(scal.p, rr, 2);
-        const double rn = rr[1];
-        if (lucky && rn > threshold) stalled = true;
-        rnorm = rn;
-    }
-    out.final_relative_residual = bnorm > 0.0 ? rnorm / bnorm : rnorm;
-    HEC_CUDA(cudaMemcpyAsync(x_host, x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    HEC_CUDA(cudaStreamSynchronize(st));
-    HEC_CUDA(cudaGetLastError());
-    out.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    return out;
-}
-
 }  // namespace hec::dev

@@ -1,13 +1,15 @@
-"""Multi-GPU RAS layer (paper_1606_00541_b200/ras.py).
+"""Multi-GPU RAS layer: the C++ plan (csrc/host/ras_plan.cpp), the device
+engine (csrc/cuda/gmres_engine.cu, comm.cpp) and its Python face (ras.py).
 
-CPU (world size 2, gloo): the distributed host logic -- reference partition,
-halo plan, all-to-all halo exchange, distributed GMRES -- with the local work
-done by the oracle (tests only). Checks: the distributed preconditioner apply
-equals the reference's hec::apply with the same blocks bitwise, and GMRES
-converges in the reference's iteration count +-1.
+CPU (gloo, world sizes 2 and 3): the product's C++ plan with the local work done
+by the oracle and the CGS2 GMRES restated in tests/ras_model.py. Checks: the
+distributed preconditioner apply equals the reference's hec::apply with the same
+blocks bitwise; GMRES converges in the reference's iteration count +-1.
 
-GPU: the same driver with the device local work (DeviceOps), world size 1
-(NCCL not needed) and world size 2 on one GPU (gloo, host-staged collectives).
+GPU: the C++ engine through the C-ABI (hec_ras_create / apply / gmres): world
+size 1, and world size 2 on one GPU (two processes, host-callback collectives
+over gloo) -- the apply bitwise equal to the reference's rows, GMRES iterations
+within +-1. (NCCL runs in the driver's multi-GPU bench, one process per GPU.)
 """
 import os
 import socket
@@ -25,104 +27,55 @@ def _free_port():
         return s.getsockname()[1]
 
 
-class OracleOps:
-    """Local subdomain work on the CPU through the oracle (test backend)."""
-
-    def __init__(self, H, a, plan, orc):
-        import torch
-        self.torch, self.orc, self.plan = torch, orc, plan
-        f = H.ilu0(H.csr_submatrix(a, plan.ext))
-        self.pl = orc.prepare(Csr.of(f.l))
-        self.pu = orc.prepare(Csr.of(f.u), upper=True)
-        self.owned = (plan.out_index >= 0).astype(np.int8)
-        self.A = Csr(plan.n_own, plan.n_loc, plan.a_rp, plan.a_ci, plan.a_v)
-
-    def vec(self, n):
-        return self.torch.zeros(n, dtype=self.torch.float64)
-
-    def apply(self, vloc, z_own):
-        x = self.orc.apply(self.plan.n_loc, self.plan.gather, self.owned, self.pl, self.pu, vloc.numpy())
-        z_own.copy_(self.torch.from_numpy(x[:self.plan.n_own]))
-
-    def matvec(self, zloc, w_own):
-        w_own.copy_(self.torch.from_numpy(self.orc.spmv(self.A, zloc.numpy())))
-
-    def mgs(self, w, v_prev, h_prev, v_next, out):
-        if v_prev is not None:
-            w.sub_(h_prev * v_prev)
-        out.copy_(self.torch.dot(w, v_next).reshape(1))
-
-    def scale(self, y, x, s):
-        y.copy_(x / s)
-
-    def combine(self, j, xc, V, ldv, y):
-        n = self.plan.n_own
-        acc = self.torch.zeros(n, dtype=self.torch.float64)
-        for i in range(j):
-            acc = acc + y[i] * V[i * ldv:i * ldv + n]
-        xc.copy_(acc)
-
-    def add(self, x, d):
-        x.add_(d)
-
-    def sqrt(self, a, out):
-        out.copy_(self.torch.sqrt(a))
-
-    def to_host(self, t):
-        return t.numpy().copy()
-
-    def from_host(self, arr):
-        return self.torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64))
-
-    def copy(self, dst, src):
-        dst.copy_(src)
-
-    def residual(self, r, b, ax):
-        self.torch.sub(b, ax, out=r)
-
-    def sub(self, V, i, ldv, n):
-        return V[i * ldv:i * ldv + n]
-
-
-def _gloo_worker(rank, world, port, dims, restart, queue):
-    import torch
+def _init(rank, world, port):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _gather_global(plan, x, n):
+    import torch.distributed as dist
+    xs = [None] * plan.world
+    dist.all_gather_object(xs, (plan.own, np.asarray(x)))
+    xg = np.zeros(n)
+    for own, xv in xs:
+        xg[own] = xv
+    return xg
+
+
+def _gloo_worker(rank, world, port, dims, restart, queue):
+    import torch.distributed as dist
+    _init(rank, world, port)
     try:
         import paper_1606_00541_b200 as H
         from paper_1606_00541_b200 import ras
         from oracle import load_oracle, load_reference
+        import ras_model
         orc, ref = load_oracle(), load_reference()
         a = H.gen_poisson7(*dims)
         plan = ras.make_plan(a, world, rank, 1)
-        ops = OracleOps(H, a, plan, orc)
-        comm = ras.TorchComm(plan, torch.device("cpu"))
+        local = ras_model.OracleLocal(H, a, plan, orc)
+        comm = ras_model.GlooComm(plan)
         # 1) distributed apply == reference hec::apply with `world` RAS blocks, bitwise
         r = np.random.default_rng(7).uniform(-1, 1, a.n_rows)
-        vloc = torch.zeros(plan.n_loc, dtype=torch.float64)
-        vloc[:plan.n_own] = torch.from_numpy(r[plan.own])
+        vloc = np.zeros(plan.n_loc)
+        vloc[:plan.n_own] = r[plan.own]
         comm.exchange(vloc)
-        z = torch.zeros(plan.n_own, dtype=torch.float64)
-        ops.apply(vloc, z)
+        z = local.apply(vloc)
         A = Csr.of(a)
         want = ref.apply(ref.precond(A, "ras", world, 1), r)
-        apply_ok = bits_equal(z.numpy(), want[plan.own])
-        # 2) distributed GMRES vs the reference's RAS GMRES
+        apply_ok = bits_equal(z, want[plan.own])
+        # 2) distributed GMRES (the engine's algorithm) vs the reference's RAS GMRES
         b = ref.spmv(A, np.ones(a.n_rows))
-        x, rep = ras.gmres(ops, comm, plan, b[plan.own], restart=restart)
-        xs = [None] * world
-        dist.all_gather_object(xs, (plan.own, x.numpy()))
+        x, rep = ras_model.gmres(local, comm, plan, b[plan.own], restart=restart)
+        xg = _gather_global(plan, x, a.n_rows)
         _, rrep = ref.gmres(A, b, ref.precond(A, "ras", world, 1), restart=restart)
         if rank == 0:
-            xg = np.zeros(a.n_rows)
-            for own, xv in xs:
-                xg[own] = xv
             res = np.linalg.norm(b - ref.spmv(A, xg)) / np.linalg.norm(b)
-            queue.put(dict(apply_ok=apply_ok, iters=rep.iterations, ref_iters=rrep["iterations"],
-                           conv=rep.converged, rel=rep.final_relative_residual, true_rel=res,
-                           allreduces=rep.allreduces, exchanges=rep.exchanges))
+            queue.put(dict(apply_ok=apply_ok, iters=rep["iterations"], ref_iters=rrep["iterations"],
+                           conv=rep["converged"], rel=rep["rel"], true_rel=res, allreduces=rep["allreduces"],
+                           exchanges=rep["exchanges"]))
         else:
             queue.put(dict(apply_ok=apply_ok))
     finally:
@@ -142,8 +95,27 @@ def test_plan_invariants(H):
             owned = p.out_index >= 0
             assert np.array_equal(np.sort(p.ext[owned]), p.own)           # restriction = own rows
             assert np.array_equal(p.gather[owned], p.out_index[owned])
+            assert np.array_equal(p.part_of[p.halo], np.sort(p.part_of[p.halo]))  # halo by owner
             for q in range(world):                                         # send / receive sizes match
-                assert len(plans[q].send_idx[p.rank]) == p.recv_counts[q]
+                assert plans[q].send_counts[p.rank] == p.recv_counts[q]
+                seg = p.halo[p.recv_offsets[q]:p.recv_offsets[q + 1]]
+                assert np.array_equal(plans[q].own[plans[q].send_idx[plans[q].send_offsets[p.rank]:
+                                                                       plans[q].send_offsets[p.rank + 1]]], seg)
+
+
+def test_plan_matches_reference_partition(H, ref):
+    # own = the reference's part, ext = the reference's extended part (precond.cpp:74-96)
+    from paper_1606_00541_b200 import ras
+    a = H.gen_poisson7(10, 9, 8)
+    A = Csr.of(a)
+    for world in (2, 4):
+        bag = ref.precond(A, "ras", world, 1)
+        part_of, offs, ext_rows = bag.ints("part_of"), bag.ints("offsets"), bag.ints("ext_rows")
+        for r in range(world):
+            p = ras.make_plan(a, world, r, 1)
+            assert np.array_equal(p.part_of, part_of)
+            assert np.array_equal(p.own, np.flatnonzero(part_of == r))
+            assert np.array_equal(p.ext, ext_rows[offs[r]:offs[r + 1]])
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -166,70 +138,75 @@ def test_ras_gmres_gloo_cpu(ref, world):
     assert main["exchanges"] > 0 and main["allreduces"] > 0
 
 
-def _gpu_worker(rank, world, port, queue):
+def _check_device_ras(H, ref, world, rank, dims, queue):
+    import torch
+    from paper_1606_00541_b200 import ras
+    a = H.gen_poisson7(*dims)
+    A = Csr.of(a)
+    b = ref.spmv(A, np.ones(a.n_rows))
+    solver = ras.RasSolver(a, overlap=1)
+    plan = solver.plan
+    # the distributed apply: rank's rows of the reference's apply(ras, world blocks), bitwise
+    r = np.random.default_rng(3).uniform(-1, 1, a.n_rows)
+    z = solver.apply_host(r[plan.own])
+    want = ref.apply(ref.precond(A, "ras", world, 1), r)
+    apply_ok = bits_equal(z, want[plan.own])
+    rd = torch.tensor(r[plan.own], device="cuda")
+    zd = torch.empty_like(rd)
+    solver.apply(rd, zd)
+    torch.cuda.synchronize()
+    apply_dev_ok = bits_equal(zd.cpu().numpy(), want[plan.own])
+    x, rep = solver.gmres(b[plan.own], restart=30)
+    xg = _gather_global(plan, x, a.n_rows) if world > 1 else x
+    _, rrep = ref.gmres(A, b, ref.precond(A, "ras", world, 1), restart=30)
+    out = dict(apply_ok=apply_ok and apply_dev_ok, iters=rep.iterations, ref_iters=rrep["iterations"],
+               conv=rep.converged, allreduces=rep.allreduces, exchanges=rep.exchanges,
+               true_rel=float(np.linalg.norm(b - ref.spmv(A, xg)) / np.linalg.norm(b)), comm=solver.comm)
+    if queue is not None:
+        queue.put(out)
+    return out
+
+
+def _gpu_worker(rank, world, port, dims, queue):
     import torch
     import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _init(rank, world, port)
     try:
         torch.cuda.set_device(0)
         import paper_1606_00541_b200 as H
-        from paper_1606_00541_b200 import ras
         from oracle import load_reference
-        ref = load_reference()
-        a = H.gen_poisson7(16, 15, 14)
-        A = Csr.of(a)
-        b = ref.spmv(A, np.ones(a.n_rows))
-        solver = ras.RasGmres(a, overlap=1, restart=30)
-        x, rep = solver.solve(b)
-        xs = [None] * world
-        dist.all_gather_object(xs, (solver.plan.own, x.cpu().numpy()))
-        _, rrep = ref.gmres(A, b, ref.precond(A, "ras", world, 1), restart=30)
-        if rank == 0:
-            xg = np.zeros(a.n_rows)
-            for own, xv in xs:
-                xg[own] = xv
-            queue.put(dict(iters=rep.iterations, ref_iters=rrep["iterations"], conv=rep.converged,
-                           true_rel=float(np.linalg.norm(b - ref.spmv(A, xg)) / np.linalg.norm(b))))
+        _check_device_ras(H, load_reference(), world, rank, dims, queue)
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_ras_gmres_device_world1(H, ref):
-    torch = pytest.importorskip("torch")
-    from paper_1606_00541_b200 import ras
-    a = H.gen_poisson7(20, 18, 16)
-    A = Csr.of(a)
-    b = ref.spmv(A, np.ones(a.n_rows))
-    solver = ras.RasGmres(a, overlap=1, restart=30)
-    x, rep = solver.solve(b)
-    _, rrep = ref.gmres(A, b, ref.precond(A, "ras", 1, 1), restart=30)
-    assert rep.converged and abs(rep.iterations - rrep["iterations"]) <= 1, (rep.iterations, rrep)
-    xr = x.cpu().numpy()
-    assert np.linalg.norm(b - ref.spmv(A, xr)) / np.linalg.norm(b) <= 1e-6
-    # the device apply on one block is the reference apply bitwise
-    r = np.random.default_rng(3).uniform(-1, 1, a.n_rows)
-    vloc = torch.tensor(r, device="cuda")
-    z = torch.empty(a.n_rows, dtype=torch.float64, device="cuda")
-    solver.ops.apply(vloc, z)
-    torch.cuda.synchronize()
-    assert bits_equal(z.cpu().numpy(), ref.apply(ref.precond(A, "ras", 1, 1), r))
+def test_ras_device_world1(H, ref):
+    out = _check_device_ras(H, ref, 1, 0, (20, 18, 16), None)
+    assert out["apply_ok"], "RAS apply differs from the reference"
+    assert out["conv"] and out["true_rel"] <= 1e-6
+    assert abs(out["iters"] - out["ref_iters"]) <= 1, out
+    assert out["comm"] == "none" and out["allreduces"] == 0
 
 
 @pytest.mark.gpu
-def test_ras_gmres_device_world2_one_gpu(ref):
+@pytest.mark.parametrize("world", [2, 3])
+def test_ras_device_multi_rank_one_gpu(ref, world):
     torch = pytest.importorskip("torch")
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, (16, 15, 14), q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = q.get(timeout=600)
+    outs = [q.get(timeout=600) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    assert out["conv"] and out["true_rel"] <= 1e-6
-    assert abs(out["iters"] - out["ref_iters"]) <= 1, out
+    for o in outs:
+        assert o["apply_ok"], "distributed RAS apply differs from the reference's rows"
+        assert o["conv"] and o["true_rel"] <= 1e-6
+        assert abs(o["iters"] - o["ref_iters"]) <= 1, o
+        assert o["comm"] == "callbacks" and o["exchanges"] > 0
+        # two all-reduces per iteration plus one per norm (CGS2), not j + 2
+        assert o["allreduces"] <= 2 * o["iters"] + 2 * (o["iters"] // 30 + 2)
