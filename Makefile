@@ -28,10 +28,17 @@ CU_OBJS   := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS))
 
 HEADERS := $(wildcard include/*.h include/hecsolve/*.hpp $(SRC)/cuda/*.hpp $(SRC)/cuda/*.cuh)
 
+BENCH_EXE := $(PKG)/bin/hecsolve_bench
+
 .PHONY: all lib oracle clean
 all: lib oracle
 
-lib: $(LIB)
+lib: $(LIB) $(BENCH_EXE)
+
+# the reference's benchmark command line (tools/bench_main.cpp) over this library
+$(BENCH_EXE): $(SRC)/tools/bench_main.cpp $(LIB) $(HEADERS)
+	@mkdir -p $(dir $@)
+	$(CXX) -O2 -std=c++20 -Iinclude -o $@ $< -L$(PKG) -lhecsolve_b200 -Wl,-rpath,'$$ORIGIN/..'
 
 $(LIB): $(HOST_OBJS) $(CAPI_OBJS) $(CU_OBJS)
 	$(NVCC) -shared $(ARCH) -cudart static -Xcompiler -fopenmp -o $@ $^ -lgomp -ldl
@@ -48,5 +55,5 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(BENCH_EXE)
 	$(MAKE) -C oracle clean

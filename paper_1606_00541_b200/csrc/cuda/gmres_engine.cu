@@ -95,10 +95,15 @@ __global__ void __launch_bounds__(kT) k_mdot(int n, const double* __restrict__ V
     for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
     const int stride = gridDim.x * kT;
     for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+        // every load of the element first (deep memory-level parallelism), then the math
+        double vk[kKG];
         const double wi = w[i];
 #pragma unroll
+        for (int k = 0; k < kKG; ++k) vk[k] = k < kc ? __ldg(V + k * ldv + i) : 0.0;
+        asm volatile("" ::: "memory");
+#pragma unroll
         for (int k = 0; k < kKG; ++k)
-            if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(__ldg(V + k * ldv + i), wi));
+            if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(vk[k], wi));
         acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(wi, wi));
     }
     reduce_out(acc, kc, with_norm, partials, counter, out);
@@ -135,14 +140,16 @@ __global__ void __launch_bounds__(kT) k_mupdate(int n, const double* __restrict_
     for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
     const int stride = gridDim.x * kT;
     for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
+        // every load of the element first (deep memory-level parallelism), then the
+        // sequential update chain
         double vk[kKG];
         double wi = w_in[i];
 #pragma unroll
+        for (int k = 0; k < kKG; ++k) vk[k] = k < kc ? __ldg(V + k * ldv + i) : 0.0;
+        asm volatile("" ::: "memory");
+#pragma unroll
         for (int k = 0; k < kKG; ++k)
-            if (k < kc) {
-                vk[k] = __ldg(V + k * ldv + i);
-                wi = __dsub_rn(wi, __dmul_rn(sc[k], vk[k]));
-            }
+            if (k < kc) wi = __dsub_rn(wi, __dmul_rn(sc[k], vk[k]));
         if (scale_mode) wi = __ddiv_rn(wi, s);
         w_out[i] = wi;
         if (with_dots) {
