@@ -102,15 +102,23 @@ int hec_tri_create(int n, int reversal_applied, int nlev, const int* level_start
  */
 int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream);
 
-/* hec_tri_solve in its two device passes: the persistent solve kernel alone
- * (b in the original order; every chunk gathers its right-hand side itself --
- * the reference's permute-in, proj/src/triangular.cpp:110-111, fused) leaves x
- * in the layout's wave order (xw[p], p = wave position; the solution order for
- * the level strategy); hec_tri_permute_out gathers x[o] = xw[wpos[o]] (the
- * reference's permute-out, proj/src/triangular.cpp:131-132). A consumer that
- * reads the wave order directly (the U solve of an ILU apply) skips the second
- * pass. b and xw must not alias. */
-int hec_tri_solve_wave(hec_tri_t t, const double* b_dev, double* xw_dev, void* stream);
+/*
+ * hec_tri_solve split in its two device passes: hec_tri_permute_in writes the
+ * right-hand side in the layout's private row order (the reference's
+ * permute-in, proj/src/triangular.cpp:110-111, into the order the persistent
+ * kernel consumes: CTA, chunk, row), then the solve from bp. That order is
+ * OPAQUE: only hec_tri_permute_in produces a valid bp. bp must hold n + 2
+ * doubles and be 16-byte aligned (the kernel moves it with bulk copies);
+ * otherwise HEC_EINVAL.
+ */
+int hec_tri_permute_in(hec_tri_t t, const double* b_dev, double* bp_dev, void* stream);
+int hec_tri_solve_ordered(hec_tri_t t, const double* bp_dev, double* x_dev, void* stream);
+/* hec_tri_solve_ordered in two halves: the solve leaves x in the layout's wave
+ * order (xw[p], p = wave position; the solution order for the level strategy),
+ * hec_tri_permute_out gathers x[o] = xw[wpos[o]] (the reference's permute-out,
+ * proj/src/triangular.cpp:131-132). A consumer that can read the wave order
+ * directly (the U solve of an ILU apply) skips the second pass. */
+int hec_tri_solve_wave(hec_tri_t t, const double* bp_dev, double* xw_dev, void* stream); /* bp: as above */
 int hec_tri_permute_out(hec_tri_t t, const double* xw_dev, double* x_dev, void* stream);
 
 /* Same with host vectors (H2D, solve, D2H; synchronous). Drop-in for hec::solve. */

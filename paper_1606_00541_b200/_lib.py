@@ -102,6 +102,8 @@ _sig("hec_device_available", c_int)
 _sig("hec_tri_create", c_int, c_int, c_int, c_int, P_int, P_int, c_int, P_int, P_dbl, P_int, P_int, P_dbl,
      C.POINTER(TriOptions), C.POINTER(c_void_p))
 _sig("hec_tri_solve", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_tri_permute_in", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
+_sig("hec_tri_solve_ordered", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
 _sig("hec_tri_solve_wave", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
 _sig("hec_tri_permute_out", c_int, c_void_p, c_void_p, c_void_p, c_void_p)
 _sig("hec_tri_solve_host", c_int, c_void_p, P_dbl, P_dbl)
@@ -192,7 +194,7 @@ _sig("hec_gmres_host", c_int, c_void_p, P_dbl, c_void_p, C.POINTER(GmresConfig),
 
 EXPORTED = [
     "hec_last_error", "hec_last_error_row", "hec_last_error_block", "hec_version", "hec_device_available",
-    "hec_tri_create", "hec_tri_solve", "hec_tri_solve_wave", "hec_tri_permute_out", "hec_tri_solve_host", "hec_tri_query", "hec_tri_destroy",
+    "hec_tri_create", "hec_tri_solve", "hec_tri_permute_in", "hec_tri_solve_ordered", "hec_tri_solve_wave", "hec_tri_permute_out", "hec_tri_solve_host", "hec_tri_query", "hec_tri_destroy",
     "hec_tri_solve_traced",
     "hec_precond_create", "hec_precond_create_local", "hec_precond_apply", "hec_precond_apply_host",
     "hec_precond_query", "hec_krylov_create", "hec_krylov_mgs", "hec_krylov_scale", "hec_krylov_combine",

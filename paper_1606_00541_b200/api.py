@@ -416,9 +416,19 @@ class DeviceTri:
         check(lib.hec_tri_solve(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(x_dev)),
                                 C.c_void_p(_stream(stream)) if stream is not None else None))
 
-    def solve_wave(self, b_dev, xw_dev, stream=None) -> None:
-        """The solve kernel alone (b in the original order), x left in the layout's wave order (see permute_out)."""
-        check(lib.hec_tri_solve_wave(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(xw_dev)),
+    def permute_in(self, b_dev, bp_dev, stream=None) -> None:
+        """bp[r] = b[input index of reordered row r]; bp holds n + 2 doubles."""
+        check(lib.hec_tri_permute_in(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(bp_dev)),
+                                     C.c_void_p(_stream(stream)) if stream is not None else None))
+
+    def solve_ordered(self, bp_dev, x_dev, stream=None) -> None:
+        """The solve from a right-hand side already in reordered-row order."""
+        check(lib.hec_tri_solve_ordered(self._h, C.c_void_p(_ptr(bp_dev)), C.c_void_p(_ptr(x_dev)),
+                                        C.c_void_p(_stream(stream)) if stream is not None else None))
+
+    def solve_wave(self, bp_dev, xw_dev, stream=None) -> None:
+        """The solve alone, x left in the layout's wave order (see permute_out)."""
+        check(lib.hec_tri_solve_wave(self._h, C.c_void_p(_ptr(bp_dev)), C.c_void_p(_ptr(xw_dev)),
                                      C.c_void_p(_stream(stream)) if stream is not None else None))
 
     def permute_out(self, xw_dev, x_dev, stream=None) -> None:

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdint>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -347,13 +348,37 @@ int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream)
     });
 }
 
-int hec_tri_solve_wave(hec_tri_t t, const double* b_dev, double* xw_dev, void* stream) {
+int hec_tri_permute_in(hec_tri_t t, const double* b_dev, double* bp_dev, void* stream) {
+    return guarded([&] {
+        need(t, "hec_tri_permute_in");
+        if (t->impl->n() > 0 && (!b_dev || !bp_dev)) throw std::invalid_argument("hec_tri_permute_in: null vector");
+        if (reinterpret_cast<std::uintptr_t>(bp_dev) & 15)
+            throw std::invalid_argument("hec_tri_permute_in: bp must be 16-byte aligned");
+        t->impl->permute(b_dev, bp_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int hec_tri_solve_ordered(hec_tri_t t, const double* bp_dev, double* x_dev, void* stream) {
+    return guarded([&] {
+        need(t, "hec_tri_solve_ordered");
+        if (t->impl->n() > 0 && (!bp_dev || !x_dev)) throw std::invalid_argument("hec_tri_solve_ordered: null vector");
+        if (bp_dev == x_dev && t->impl->n() > 0)
+            throw std::invalid_argument("hec_tri_solve_ordered: bp and x must not alias");
+        if (reinterpret_cast<std::uintptr_t>(bp_dev) & 15)
+            throw std::invalid_argument("hec_tri_solve_ordered: bp must be 16-byte aligned");
+        t->impl->solve_ordered(bp_dev, x_dev, nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int hec_tri_solve_wave(hec_tri_t t, const double* bp_dev, double* xw_dev, void* stream) {
     return guarded([&] {
         need(t, "hec_tri_solve_wave");
-        if (t->impl->n() > 0 && (!b_dev || !xw_dev)) throw std::invalid_argument("hec_tri_solve_wave: null vector");
-        if (b_dev == xw_dev && t->impl->n() > 0)
-            throw std::invalid_argument("hec_tri_solve_wave: b and xw must not alias");
-        t->impl->solve_wave(b_dev, xw_dev, nullptr, static_cast<cudaStream_t>(stream));
+        if (t->impl->n() > 0 && (!bp_dev || !xw_dev)) throw std::invalid_argument("hec_tri_solve_wave: null vector");
+        if (bp_dev == xw_dev && t->impl->n() > 0)
+            throw std::invalid_argument("hec_tri_solve_wave: bp and xw must not alias");
+        if (reinterpret_cast<std::uintptr_t>(bp_dev) & 15)
+            throw std::invalid_argument("hec_tri_solve_wave: bp must be 16-byte aligned");
+        t->impl->solve_wave(bp_dev, xw_dev, nullptr, static_cast<cudaStream_t>(stream));
     });
 }
 

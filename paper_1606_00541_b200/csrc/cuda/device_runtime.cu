@@ -172,7 +172,7 @@ DeviceTri::~DeviceTri() {
 
 int DeviceTri::launches_per_solve() const {
     if (n_ == 0) return 0;
-    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 2;  // wave (gathers b) + permute-out
+    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 3;  // permute-in + wave + permute-out
 }
 
 DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
@@ -184,11 +184,18 @@ DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
         const uint32_t init[3] = {0u, 0u, 1u};
         HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
         w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
+        w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
         w->xw.alloc(static_cast<std::size_t>(std::max(n_, 1)));
         HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
         HEC_CUDA(cudaDeviceSynchronize());
     }
     return *w;
+}
+
+void DeviceTri::permute(const double* b, double* bp, cudaStream_t st) const {
+    if (n_ == 0) return;
+    permute_in(b, strategy_ == 1 ? l_bidx_.p : p_bidx_.p, bp, n_, st);
+    HEC_CUDA(cudaGetLastError());
 }
 
 void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st, unsigned long long* trace) {
@@ -198,8 +205,8 @@ void DeviceTri::solve(const double* b, double* xs, double* out, cudaStream_t st,
         return;
     }
     Workspace& w = workspace(st);
-    solve_wave(b, w.xw.p, out, st, trace);  // each chunk gathers its b (fused permute-in)
-    permute_out(w.xw.p, xs, st);
+    permute(b, w.bp.p, st);
+    solve_ordered(w.bp.p, xs, out, st, trace);
 }
 void DeviceTri::permute_out(const double* xw, double* xs, cudaStream_t st) const {
     if (n_ == 0 || !xs) return;
@@ -234,10 +241,20 @@ void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* ou
     }
 }
 
-void DeviceTri::solve_wave(const double* b, double* xw, double* out, cudaStream_t st, unsigned long long* trace) {
+void DeviceTri::solve_ordered(const double* bp, double* xs, double* out, cudaStream_t st, unsigned long long* trace) {
     if (n_ == 0) return;
     if (strategy_ == 1) {
-        run_levels(b, false, xw, out, st);
+        run_levels(bp, true, xs, out, st);
+        return;
+    }
+    Workspace& w = workspace(st);
+    solve_wave(bp, w.xw.p, out, st, trace);
+    permute_out(w.xw.p, xs, st);
+}
+void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream_t st, unsigned long long* trace) {
+    if (n_ == 0) return;
+    if (strategy_ == 1) {
+        run_levels(bp, true, xw, out, st);
         return;
     }
     Workspace& w = workspace(st);
@@ -245,8 +262,7 @@ void DeviceTri::solve_wave(const double* b, double* xw, double* out, cudaStream_
     a.blobs = p_blob_.p;
     a.spans = reinterpret_cast<const int4*>(p_spans_.p);
     a.cta_chunk0 = p_cta0_.p;
-    a.b = b;
-    a.bidx = p_bidx_.p;
+    a.bp = bp;
     a.xs = xw;
     a.out = has_out_ ? out : nullptr;
     a.mbox = w.mailbox.p;
@@ -303,9 +319,8 @@ DevicePrecond::DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, 
     l.b_map = gather;
     u.out_map = out_index;
     l_ = std::make_unique<DeviceTri>(l, opt);
-    const std::vector<int>& wl = l_->host_wpos();  // U reads L's output where L left it (wave order)
-    if (!wl.empty()) u.b_map = wl.data();
     u_ = std::make_unique<DeviceTri>(u, opt);
+    compose();
 }
 
 DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
@@ -331,9 +346,8 @@ DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* ow
         u.out_map = out_map.data(); // U scatters owned rows into x
     }
     l_ = std::make_unique<DeviceTri>(l, opt);
-    const std::vector<int>& wl = l_->host_wpos();  // U reads L's output where L left it (wave order)
-    if (!wl.empty()) u.b_map = wl.data();
     u_ = std::make_unique<DeviceTri>(u, opt);
+    compose();
 }
 
 DevicePrecond::~DevicePrecond() {
@@ -345,7 +359,9 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
     auto& w = ws_[st];
     if (!w) {
         w = std::make_unique<Workspace>();
+        w->bl.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
         w->yw.alloc(std::max(n_ext_, 1));
+        w->bu.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
         w->xw.alloc(std::max(n_ext_, 1));
     }
     return *w;
@@ -354,17 +370,26 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
 void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
     if (n_ext_ == 0) return;
     Workspace& w = workspace(st);
-    // L gathers r through its map (chunk by chunk, inside the kernel) and leaves
-    // its output in wave order; U gathers its right-hand side straight from there
-    // (its source map is composed with L's wave positions at construction): two
-    // persistent kernels, no permutation passes between them
-    l_->solve_wave(r, w.yw.p, nullptr, st);
+    // L from r gathered into its row order, its output left in wave order; U's
+    // right-hand side is gathered straight from there through the composed map
+    // (no pass through the solution order in between)
+    l_->permute(r, w.bl.p, st);
+    l_->solve_wave(w.bl.p, w.yw.p, nullptr, st);
+    permute_in(w.yw.p, lu_map_.p, w.bu.p, n_ext_, st);
+    HEC_CUDA(cudaGetLastError());
     if (identity_) {
-        u_->solve_wave(w.yw.p, w.xw.p, nullptr, st);
+        u_->solve_wave(w.bu.p, w.xw.p, nullptr, st);
         u_->permute_out(w.xw.p, x, st);
     } else {
-        u_->solve_wave(w.yw.p, w.xw.p, x, st);  // owned rows scattered into x by the kernel
+        u_->solve_wave(w.bu.p, w.xw.p, x, st);  // owned rows scattered into x by the kernel
     }
+}
+void DevicePrecond::compose() {
+    const std::vector<int>& bu = u_->host_bidx();
+    const std::vector<int>& wl = l_->host_wpos();
+    std::vector<int> m(static_cast<std::size_t>(n_ext_));
+    for (int p = 0; p < n_ext_; ++p) m[p] = wl.empty() ? bu[p] : wl[bu[p]];
+    lu_map_.upload(m);
 }
 
 cudaStream_t DevicePrecond::host_stream(std::unique_lock<std::mutex>& lock) {
@@ -375,12 +400,7 @@ cudaStream_t DevicePrecond::host_stream(std::unique_lock<std::mutex>& lock) {
 
 int DevicePrecond::launches_per_apply() const {
     if (n_ext_ == 0) return 0;
-    // one persistent kernel per wave triangle (one launch per level otherwise), plus
-    // the permute-out of a full (identity) apply whose U is a wave layout
-    auto solve_launches = [](const DeviceTri& t) {
-        return t.stats().strategy == 1 ? t.launches_per_solve() : 1;
-    };
-    return solve_launches(*l_) + solve_launches(*u_) + (identity_ && u_->stats().strategy == 2 ? 1 : 0);
+    return l_->launches_per_solve() + u_->launches_per_solve() - (identity_ ? 1 : 2);
 }
 
 void DevicePrecond::apply_host(const double* r, double* x) {

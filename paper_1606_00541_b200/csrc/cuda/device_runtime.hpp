@@ -81,10 +81,14 @@ public:
     // xs[o] = solution; out[oidx] = solution where oidx >= 0 (if out != null).
     void solve(const double* b, double* xs, double* out, cudaStream_t st,
                unsigned long long* trace = nullptr);
-    // The solve alone (b in input order, gathered chunk by chunk inside the
-    // kernel): x in *wave order* (xw[wave position]; the solution order for the
-    // level strategy), then permute_out gives xs[o] = xw[wpos[o]].
-    void solve_wave(const double* b, double* xw, double* out, cudaStream_t st,
+    // The two halves of solve(): bp[r] = b[bidx[r]] (bp holds n + 2 doubles), then
+    // the solve from the reordered right-hand side.
+    void permute(const double* b, double* bp, cudaStream_t st) const;
+    void solve_ordered(const double* bp, double* xs, double* out, cudaStream_t st,
+                       unsigned long long* trace = nullptr);
+    // The solve alone: x in *wave order* (xw[wave position]; the solution order for
+    // the level strategy), then permute_out gives xs[o] = xw[wpos[o]].
+    void solve_wave(const double* bp, double* xw, double* out, cudaStream_t st,
                     unsigned long long* trace = nullptr);
     void permute_out(const double* xw, double* xs, cudaStream_t st) const;
     // host copies of the maps: bidx (reordered input) and wpos (solution index ->
@@ -103,6 +107,7 @@ private:
     struct Workspace {
         DevBuf<uint32_t> counters;            // ticket, finished CTAs, mailbox epoch
         DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
+        DevBuf<double> bp;                    // right-hand side in reordered-row order
         DevBuf<double> xw;                    // solution in wave order
     };
     Workspace& workspace(cudaStream_t st);
@@ -159,11 +164,13 @@ public:
 
 private:
     struct Workspace {
-        DevBuf<double> yw, xw;  // L output (wave order), U output (wave order)
+        DevBuf<double> bl, yw, bu, xw;  // L input (reordered), L output (wave), U input, U output
     };
     int n_ = 0, n_out_ = 0, n_ext_ = 0;
     bool identity_ = true;
     std::unique_ptr<DeviceTri> l_, u_;
+    DevBuf<int> lu_map_;  // U input position -> L output position (the two permutations composed)
+    void compose();
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
     std::mutex h_mu_;

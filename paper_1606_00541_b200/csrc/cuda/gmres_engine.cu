@@ -36,6 +36,7 @@
 #include "comm.hpp"
 #include "device_runtime.hpp"
 #include "gmres_engine.hpp"
+#include "ptx.cuh"
 
 namespace hec::dev {
 
@@ -86,90 +87,112 @@ __device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int w
     if (threadIdx.x == 0) *counter = 0;
 }
 
-// out[k] = V_k . w for k < kc (kc <= kKG); with_norm: out[kc] = w . w.
-__global__ void __launch_bounds__(kT) k_mdot(int n, const double* __restrict__ V, size_t ldv, int kc,
-                                             const double* __restrict__ w, int with_norm, double* partials,
-                                             unsigned* counter, double* out) {
-    double acc[kMaxOut];
-#pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
-    const int stride = gridDim.x * kT;
-    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
-        // every load of the element first (deep memory-level parallelism), then the math
-        double vk[kKG];
-        const double wi = w[i];
-#pragma unroll
-        for (int k = 0; k < kKG; ++k) vk[k] = k < kc ? __ldg(V + k * ldv + i) : 0.0;
-        asm volatile("" ::: "memory");
-#pragma unroll
-        for (int k = 0; k < kKG; ++k)
-            if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(vk[k], wi));
-        acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(wi, wi));
-    }
-    reduce_out(acc, kc, with_norm, partials, counter, out);
+// Multi-vector kernel (the Gram-Schmidt passes, the basis combination and the
+// norms): every block streams row tiles of kc basis columns (and w) into shared
+// memory with TMA bulk copies, double-buffered on mbarriers, so the memory
+// system always has two tiles per SM in flight while the threads work from
+// shared memory (one row per thread):
+//   w_out = (w_in - sum_{k<kc} c_k V_k) / s      if w_out (w_in null: 0.0;
+//            k in order; s per scale_mode: 0 none, 1 scale_val, 2 the CGS2 norm
+//            sqrt(max(0, c[kc] - sum_k c_k^2)) written to *s_out)
+//   out[k] = V_k . u (k < kc), out[kc] = u . u   if dots (u = w_out, or w_in
+//            when nothing is written; the norm only if with_norm)
+constexpr int kTile = 256;  // rows per tile = threads per block
+struct MvArgs {
+    int n, kc;
+    size_t ldv;
+    const double* V;
+    const double* c;
+    const double* w_in;
+    double* w_out;
+    int scale_mode;
+    double scale_val;
+    double* s_out;
+    int dots, with_norm;
+    double* partials;
+    unsigned* counter;
+    double* out;
+};
+
+// Called by the 32 lanes of warp 0: lane 0 arms the stage's mbarrier with the
+// tile's byte count, then every lane issues the bulk copies of its columns (a
+// single thread issuing ~30 copies back to back would pace the stream).
+__device__ __forceinline__ void mv_issue(const MvArgs& a, int tile, double* stage, uint64_t* bar, int lane) {
+    const int r0 = tile * kTile;
+    const int m = min(kTile, a.n - r0);
+    const uint32_t bytes = static_cast<uint32_t>(((m + 1) & ~1) * 8);  // 16-byte multiple (columns are padded)
+    const int nw = a.w_in ? 1 : 0;
+    if (lane == 0) mbar_expect_tx(bar, bytes * static_cast<uint32_t>(a.kc + nw));
+    __syncwarp();
+    for (int k = lane; k < a.kc + nw; k += 32)
+        bulk_g2s(stage + k * kTile, k < a.kc ? a.V + k * a.ldv + r0 : a.w_in + r0, bytes, bar);
 }
 
-// w_out = (w_in - sum_{k<kc} c_k V_k) / s  (k in order; s = 1 unless scaled), where
-//   scale_mode 0: no scaling
-//   scale_mode 1: s = scale_val
-//   scale_mode 2: s = sqrt(max(0, c[kc] - sum_k c_k^2)) (the CGS2 norm), written to *s_out
-// with_dots: out[k] = V_k . w_out (k < kc), out[kc] = w_out . w_out.
-__global__ void __launch_bounds__(kT) k_mupdate(int n, const double* __restrict__ V, size_t ldv, int kc,
-                                                const double* __restrict__ c, const double* w_in, double* w_out,
-                                                int scale_mode, double scale_val, double* s_out, int with_dots,
-                                                double* partials, unsigned* counter, double* out) {
+__global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
+    extern __shared__ __align__(128) double mv_smem[];
+    __shared__ uint64_t bar[2];
     __shared__ double sc[kMaxOut];
     __shared__ double s_scale;
-    if (threadIdx.x < kc) sc[threadIdx.x] = c[threadIdx.x];
-    if (threadIdx.x == 0) {
+    const int tid = threadIdx.x;
+    const int ntiles = (a.n + kTile - 1) / kTile;
+    const int per_stage = (a.kc + 1) * kTile;
+    if (tid < a.kc && a.c) sc[tid] = a.c[tid];
+    if (tid == 0) {
         double s = 1.0;
-        if (scale_mode == 1) s = scale_val;
-        if (scale_mode == 2) {
+        if (a.scale_mode == 1) s = a.scale_val;
+        if (a.scale_mode == 2) {
             double h2 = 0.0;
-            for (int k = 0; k < kc; ++k) h2 = __dadd_rn(h2, __dmul_rn(c[k], c[k]));
-            s = __dsqrt_rn(fmax(__dsub_rn(c[kc], h2), 0.0));
-            if (blockIdx.x == 0) *s_out = s;
+            for (int k = 0; k < a.kc; ++k) h2 = __dadd_rn(h2, __dmul_rn(a.c[k], a.c[k]));
+            s = __dsqrt_rn(fmax(__dsub_rn(a.c[a.kc], h2), 0.0));
+            if (blockIdx.x == 0) *a.s_out = s;
             if (!(s > 0.0)) s = 1.0;  // breakdown: the column is never used (gmres.cpp:79-83)
         }
         s_scale = s;
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (tid < 32)
+        for (int q = 0; q < 2; ++q) {
+            const int tile = blockIdx.x + q * gridDim.x;
+            if (tile < ntiles) mv_issue(a, tile, mv_smem + q * per_stage, &bar[q], tid);
+        }
     const double s = s_scale;
     double acc[kMaxOut];
 #pragma unroll
     for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
-    const int stride = gridDim.x * kT;
-    for (int i = blockIdx.x * kT + threadIdx.x; i < n; i += stride) {
-        // every load of the element first (deep memory-level parallelism), then the
-        // sequential update chain
-        double vk[kKG];
-        double wi = w_in[i];
+    for (int it = 0, tile = blockIdx.x; tile < ntiles; ++it, tile += gridDim.x) {
+        const int q = it & 1;
+        const double* st = mv_smem + q * per_stage;
+        mbar_wait(&bar[q], (it >> 1) & 1);
+        const int i = tile * kTile + tid;
+        if (i < a.n) {
+            double u = a.w_in ? st[a.kc * kTile + tid] : 0.0;
+            if (a.w_out) {
 #pragma unroll
-        for (int k = 0; k < kKG; ++k) vk[k] = k < kc ? __ldg(V + k * ldv + i) : 0.0;
-        asm volatile("" ::: "memory");
+                for (int k = 0; k < kKG; ++k)
+                    if (k < a.kc) u = __dsub_rn(u, __dmul_rn(sc[k], st[k * kTile + tid]));
+                if (a.scale_mode) u = __ddiv_rn(u, s);
+                a.w_out[i] = u;
+            }
+            if (a.dots) {
 #pragma unroll
-        for (int k = 0; k < kKG; ++k)
-            if (k < kc) wi = __dsub_rn(wi, __dmul_rn(sc[k], vk[k]));
-        if (scale_mode) wi = __ddiv_rn(wi, s);
-        w_out[i] = wi;
-        if (with_dots) {
-#pragma unroll
-            for (int k = 0; k < kKG; ++k)
-                if (k < kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(vk[k], wi));
-            acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(wi, wi));
+                for (int k = 0; k < kKG; ++k)
+                    if (k < a.kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(st[k * kTile + tid], u));
+                acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(u, u));
+            }
+        }
+        __syncthreads();  // every thread is done with this stage
+        if (tid < 32) {
+            const int next = tile + 2 * gridDim.x;
+            if (next < ntiles) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+                mv_issue(a, next, mv_smem + q * per_stage, &bar[q], tid);
+            }
         }
     }
-    if (!with_dots) return;
-    reduce_out(acc, kc, 1, partials, counter, out);
-}
-
-// xc = sum_{i<j} y_i V_i, accumulated in i order from 0.0 (gmres.cpp:121-122)
-__global__ void k_combine_v(int n, int j, double* xc, const double* V, size_t ldv, const double* y) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int i = 0; i < j; ++i) s = __dadd_rn(s, __dmul_rn(y[i], V[i * ldv + t]));
-        xc[t] = s;
-    }
+    if (a.dots) reduce_out(acc, a.kc, a.with_norm, a.partials, a.counter, a.out);
 }
 
 __global__ void k_add_v(int n, double* x, const double* d) {
@@ -219,11 +242,12 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     const int mr = cfg.restart;
     GmresOutcome out;
     const int grid = std::max(1, std::min(4 * sm_count(), (n + kT - 1) / kT));
+    const int sms = sm_count();
     const size_t ldv = static_cast<size_t>((std::max(S.n_loc, 1) + 31) / 32 * 32);  // 256-byte aligned columns
 
     DevBuf<double> V(static_cast<size_t>(mr + 1) * ldv), w(ldv), zloc(ldv), xloc(ldv), xc(ldv), r(ldv), b(ldv);
     DevBuf<double> hb(2 * static_cast<size_t>(mr) + 8), yv(static_cast<size_t>(mr) + 1);
-    DevBuf<double> partials(static_cast<size_t>(kMaxOut) * grid), sendbuf(std::max(S.n_send, 1));
+    DevBuf<double> partials(static_cast<size_t>(kMaxOut) * 8 * sms), sendbuf(std::max(S.n_send, 1));
     DevBuf<unsigned> counter(1);
     HEC_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), st));
     HEC_CUDA(cudaMemsetAsync(xloc.p, 0, sizeof(double) * ldv, st));
@@ -249,9 +273,41 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         }
         ++out.launches;
     };
-    auto norm = [&](const double* v) {  // sqrt(sum over ranks of v . v)
-        k_mdot<<<grid, kT, 0, st>>>(n, nullptr, ldv, 0, v, 1, partials.p, counter.p, hb.p);
+    // one multi-vector pass (k_mv): grid sized by the shared memory its tiles need
+    static bool mv_attr = false;
+    if (!mv_attr) {
+        HEC_CUDA(cudaFuncSetAttribute(k_mv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      2 * kMaxOut * kTile * static_cast<int>(sizeof(double))));
+        mv_attr = true;
+    }
+    auto mv = [&](int kc, const double* Vb, const double* c, const double* w_in, double* w_out, int scale_mode,
+                  double scale_val, double* s_out, int dots, int with_norm, double* outp) {
+        MvArgs m{};
+        m.n = n;
+        m.kc = kc;
+        m.ldv = ldv;
+        m.V = Vb;
+        m.c = c;
+        m.w_in = w_in;
+        m.w_out = w_out;
+        m.scale_mode = scale_mode;
+        m.scale_val = scale_val;
+        m.s_out = s_out;
+        m.dots = dots;
+        m.with_norm = with_norm;
+        m.partials = partials.p;
+        m.counter = counter.p;
+        m.out = outp;
+        const int smem = 2 * (kc + 1) * kTile * static_cast<int>(sizeof(double));
+        const int per_sm = std::max(1, std::min(8, (227 * 1024) / (smem + 2048)));
+        const int ntiles = (n + kTile - 1) / kTile;
+        const int g = std::max(1, std::min(ntiles, per_sm * sms));
+        k_mv<<<g, kTile, smem, st>>>(m);
+        HEC_CUDA(cudaGetLastError());
         ++out.launches;
+    };
+    auto norm = [&](const double* v) {  // sqrt(sum over ranks of v . v)
+        mv(0, nullptr, nullptr, v, nullptr, 0, 1.0, nullptr, 1, 1, hb.p);
         comm.allreduce_sum(hb.p, 1, st);
         double s2 = 0.0;
         HEC_CUDA(cudaMemcpyAsync(&s2, hb.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -261,7 +317,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
 
     const double bnorm = norm(b.p);
     const double threshold = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
-    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr);
+    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr), ny(mr + 1);
     HEC_CUDA(cudaMemcpyAsync(r.p, b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     double rnorm = bnorm;
     bool stalled = false;
@@ -273,9 +329,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         }
         if (out.iterations >= cfg.max_iters || stalled) break;
         // v_0 = r / rnorm (gmres.cpp:62)
-        k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, 0, hb.p, r.p, V.p, 1, rnorm, nullptr, 0, partials.p, counter.p,
-                                       nullptr);
-        ++out.launches;
+        mv(0, nullptr, nullptr, r.p, V.p, 1, rnorm, nullptr, 0, 0, nullptr);
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = rnorm;
 
@@ -287,31 +341,24 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
             const int kc = j + 1;
             if (kc <= kKG) {
                 // CGS2 pass 1: h1 = V^T w
-                k_mdot<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, w.p, 0, partials.p, counter.p, hb1);
+                mv(kc, V.p, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 0, hb1);
                 comm.allreduce_sum(hb1, kc, st);
                 // pass 2: w' = w - V h1; h2 = V^T w', ||w'||^2
-                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, hb1, w.p, w.p, 0, 1.0, nullptr, 1, partials.p,
-                                               counter.p, hb2);
+                mv(kc, V.p, hb1, w.p, w.p, 0, 1.0, nullptr, 1, 1, hb2);
                 comm.allreduce_sum(hb2, kc + 1, st);
                 // v_{j+1} = (w' - V h2) / ||w''||
-                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, kc, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0,
-                                               hb2 + kc + 1, 0, partials.p, counter.p, nullptr);
-                out.launches += 3;
+                mv(kc, V.p, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
             } else {
                 // more basis vectors than one fused pass holds: modified Gram-Schmidt,
                 // one vector at a time (each step still one dot + one all-reduce)
                 for (int i = 0; i < kc; ++i) {
-                    k_mdot<<<grid, kT, 0, st>>>(n, V.p + i * ldv, ldv, 1, w.p, 0, partials.p, counter.p, hb1 + i);
+                    mv(1, V.p + i * ldv, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 0, hb1 + i);
                     comm.allreduce_sum(hb1 + i, 1, st);
-                    k_mupdate<<<grid, kT, 0, st>>>(n, V.p + i * ldv, ldv, 1, hb1 + i, w.p, w.p, 0, 1.0, nullptr,
-                                                   i + 1 == kc, partials.p, counter.p, hb2 + kc - 1);
-                    out.launches += 2;
+                    mv(1, V.p + i * ldv, hb1 + i, w.p, w.p, 0, 1.0, nullptr, i + 1 == kc, 1, hb2 + kc - 1);
                 }
                 comm.allreduce_sum(hb2 + kc, 1, st);
                 HEC_CUDA(cudaMemsetAsync(hb2, 0, sizeof(double) * kc, st));
-                k_mupdate<<<grid, kT, 0, st>>>(n, V.p, ldv, 0, hb2 + kc, w.p, V.p + (j + 1) * ldv, 2, 1.0,
-                                               hb2 + kc + 1, 0, partials.p, counter.p, nullptr);
-                ++out.launches;
+                mv(0, nullptr, hb2 + kc, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
             }
             HEC_CUDA(cudaMemcpyAsync(hh.data(), hb.p, sizeof(double) * (2 * mr + 8), cudaMemcpyDeviceToHost, st));
             HEC_CUDA(cudaStreamSynchronize(st));
@@ -355,9 +402,13 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
             for (int t = i + 1; t < j; ++t) s -= h[i + t * (mr + 1)] * y[t];
             y[i] = s / h[i + i * (mr + 1)];
         }
-        HEC_CUDA(cudaMemcpyAsync(yv.p, y.data(), sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
-        k_combine_v<<<grid, kT, 0, st>>>(n, j, xc.p, V.p, ldv, yv.p);
-        ++out.launches;
+        // xc = sum_i y_i V_i from 0.0 in i order (gmres.cpp:121-122) as 0 - sum (-y_i) V_i (exact negation)
+        for (int i = 0; i < j; ++i) ny[i] = -y[i];
+        HEC_CUDA(cudaMemcpyAsync(yv.p, ny.data(), sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
+        HEC_CUDA(cudaStreamSynchronize(st));  // ny is reused next cycle
+        for (int k0 = 0; k0 < std::max(j, 1); k0 += kKG)  // groups of at most kKG columns, k order kept
+            mv(std::min(kKG, j - k0), V.p + k0 * ldv, yv.p + k0, k0 ? xc.p : nullptr, xc.p, 0, 1.0, nullptr, 0, 0,
+               nullptr);
         if (S.M) {
             halo(xc.p);
             S.M->apply(xc.p, zloc.p, st);

@@ -27,11 +27,10 @@ struct LevelArgs {
 
 struct WaveArgs {
     const unsigned char* blobs;  // all chunk blobs (16-byte aligned)
-    const int4* spans;           // 2 per chunk: (blob offset / 16, blob bytes, region position, r0),
-                                 //              (b area bytes, rows m, chunk to wait for, 0)
+    const int4* spans;           // 2 per chunk: (blob offset / 16, blob bytes, region bytes, r0),
+                                 //              (b area bytes, b copy bytes, 0, 0)
     const int* cta_chunk0;       // ctas + 1
-    const double* b;             // right-hand side (input order; each chunk gathers b[bidx[r0 + t]])
-    const int* bidx;             // wave position -> index into b
+    const double* bp;            // right-hand side in reordered-row order
     double* xs;
     double* out;
     unsigned long long* mbox;    // 2 words per exported row: {lo32|epoch<<32, hi32|epoch<<32}
@@ -58,7 +57,6 @@ void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
-constexpr int kWaveMaxRowsPerLane = 16;                // rows per chunk <= 32 x 16 (G x 32 x RPL <= 512)
 constexpr int kWaveProducers = 2;                      // producer warps (chunks round robin)
 constexpr int kWaveWaiters = 5;                        // waiter warps (3 could not keep up with 27-point halos)
 constexpr int kWaveRoleThreads = 32 * (kWaveProducers + kWaveWaiters);

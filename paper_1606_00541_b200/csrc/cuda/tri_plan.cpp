@@ -369,9 +369,6 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         P.rpl = 2;
     }
 
-    if (NW * warp_rows > 512)  // the producer gathers at most 16 rows of b per lane (kWaveMaxRowsPerLane)
-        throw std::invalid_argument("hec_tri_create: solver shape holds more than 512 rows per chunk");
-
     // 1. chunk discovery: per level, each CTA's rows (ordered by warp, then by
     //    row, so every warp's rows are one segment), split so that no warp has
     //    more than warp_rows rows in a chunk and by bytes
@@ -662,14 +659,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             st_hval[c] += nhalo;
             (void)any_exp;  // the export list is always present (-1 = row not exported)
             const long long wpos = cta_wbase[c] + q0;  // wave position of the chunk's first row
-            const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0);
+            const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0) |
+                              ((wpos & 1) ? 32 : 0);
             const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
             const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
             out.resize(base + round_up(sec.end, 16), 0);
             unsigned char* b = out.data() + base;
-            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, hq0[c][j], static_cast<int>(wpos),
-                                 0, 0, 0};
+            const WaveHeader hdr{m, mp, q0, flags, nhalo, sec.halo, sec.tptr, hq0[c][j], static_cast<int>(wpos), 0, 0, 0};
             std::memcpy(b, &hdr, sizeof(hdr));
             for (int wi = 0; wi < NW; ++wi) {
                 const unsigned a = t0[wi] < 0 ? 0u : (static_cast<unsigned>(t0[wi]) | (static_cast<unsigned>(t1[wi]) << 16));
@@ -711,7 +708,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             sp[2] = region;
             sp[3] = static_cast<int>(wpos);
             sp[4] = wave_b_area(m);
-            sp[5] = m;  // rows: the producer gathers their b through bidx
+            sp[5] = round_up(8 * (m + static_cast<int>(wpos & 1)), 16);
         }
     }
     for (int c = 0; c < C; ++c)

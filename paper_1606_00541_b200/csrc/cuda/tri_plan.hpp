@@ -98,12 +98,12 @@ LevelLayout build_levels(const TriSource& s);
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
 //   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages,
 //                                  in (ELL slot, row) order of first use
-// The chunk's right-hand side is gathered by the producer warp with
-// asynchronous 8-byte copies, b[bidx[r0 + t]] (bidx: wave position -> input
-// index, b_map[o] or o) straight into the region: the reference's permute-in
-// pass (triangular.cpp:110-111) fused into the solve, no permuted copy in HBM.
-// The shared-memory region of a chunk is [b: 8*mb][blob], mb = round_up(m + 1, 4).
-// Regions are placed in the byte ring by the host (span).
+// The right-hand side arrives permuted into wave order (bp[p] = b[bidx[p]],
+// one coalesced pass before the solve), so a chunk's b values are one
+// contiguous range that a second bulk copy moves next to the blob. The
+// shared-memory region of a chunk is [b: 8*mb][blob], mb = round_up(m + 1, 4);
+// b starts one element in when r0 is odd (flags&32, the copy source is rounded
+// down to 16 bytes). Regions are placed in the byte ring by the host (span).
 struct WaveConfig {
     int ctas = 148;
     int group = 0;            // solver warps per chunk (G); 0 = auto from the rows per (CTA, level)
@@ -151,7 +151,7 @@ struct WaveSections {
 
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
-    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo
+    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0
     int nhalo, halo, tptr, hq0;    // halo id list / tail offsets, halo ring position of the first staged value
     int r0, pad0, pad1, pad2;      // wave position of the chunk's first row (where its x values go)
 };

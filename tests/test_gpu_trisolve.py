@@ -162,8 +162,8 @@ def test_empty_and_single(H):
 
 
 @pytest.mark.parametrize("strategy", STRATS)
-def test_wave_solve_then_permute_out(H, orc, strategy):
-    # hec_tri_solve_wave (b gathered inside the kernel) + hec_tri_permute_out == hec_tri_solve, bitwise
+def test_permute_in_then_ordered_solve(H, orc, strategy):
+    # hec_tri_permute_in + hec_tri_solve_ordered == hec_tri_solve, bitwise
     torch = pytest.importorskip("torch")
     for gen, dims in (("gen_poisson7", (20, 17, 9)), ("gen_poisson27", (9, 8, 7))):
         a = getattr(H, gen)(*dims)
@@ -175,10 +175,10 @@ def test_wave_solve_then_permute_out(H, orc, strategy):
             b = rng.uniform(-1, 1, a.n_rows)
             want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
             bd = torch.tensor(b, device="cuda")
-            xw = torch.full_like(bd, float("nan"))
+            bp = torch.full((a.n_rows + 2,), float("nan"), dtype=torch.float64, device="cuda")
             x = torch.empty_like(bd)
-            t.solve_wave(bd, xw)
-            t.permute_out(xw, x)
+            t.permute_in(bd, bp)
+            t.solve_ordered(bp, x)
             torch.cuda.synchronize()
             assert bits_equal(x.cpu().numpy(), want)
 
@@ -292,9 +292,11 @@ def test_wave_order_output(H, orc, strategy):
         b = rng.uniform(-1, 1, a.n_rows)
         want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
         bd = torch.tensor(b, device="cuda")
+        bp = torch.empty(a.n_rows + 2, dtype=torch.float64, device="cuda")
         xw = torch.empty_like(bd)
         x = torch.full_like(bd, float("nan"))
-        t.solve_wave(bd, xw)
+        t.permute_in(bd, bp)
+        t.solve_wave(bp, xw)
         t.permute_out(xw, x)
         torch.cuda.synchronize()
         assert bits_equal(x.cpu().numpy(), want)
