@@ -8,6 +8,7 @@
 #include "tri_plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <cstring>
 #include <stdexcept>
@@ -557,9 +558,12 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 for_each_entry(s, r, [&](int col, double) {
                     if (owner_r[col] != owner_r[r]) exported[col] = 1;  // benign race: all write 1
                 });
+        // ids in wave order: the exported rows of a chunk get consecutive mailboxes
+        std::vector<int> r_of_p(n);
+        for (int r = 0; r < n; ++r) r_of_p[wpos_r[r]] = r;
         long long e = 0;
-        for (int r = 0; r < n; ++r)
-            if (exported[r]) export_id[r] = static_cast<int>(e++);
+        for (int p = 0; p < n; ++p)
+            if (exported[r_of_p[p]]) export_id[r_of_p[p]] = static_cast<int>(e++);
         if (e > 0x7ffffffeLL) throw std::overflow_error("hec_tri_create: too many exported rows");
         P.exports = e;
     }
@@ -659,8 +663,13 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             st_hval[c] += nhalo;
             (void)any_exp;  // the export list is always present (-1 = row not exported)
             const long long wpos = cta_wbase[c] + q0;  // wave position of the chunk's first row
+            bool unit = true;  // every diagonal exactly 1.0 (ILU(0) L): no diag section, no division
+            for (int t = 0; t < m && unit; ++t) {
+                const int r = cta_rows[c][ch.row0 + t];
+                unit = s.csr_vals[s.csr_rp[r + 1] - 1] == 1.0 && !std::signbit(s.csr_vals[s.csr_rp[r + 1] - 1]);
+            }
             const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0) |
-                              ((wpos & 1) ? 32 : 0);
+                              ((wpos & 1) ? 32 : 0) | (unit ? 64 : 0);
             const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
             const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
@@ -676,17 +685,32 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             if (nhalo) std::memcpy(b + sec.halo, halo.data(), 4 * nhalo);
             auto put_i = [&](int off, int idx, int v) { std::memcpy(b + off + 4 * idx, &v, 4); };
             auto put_d = [&](int off, int idx, double v) { std::memcpy(b + off + 8 * idx, &v, 8); };
+            int ebase = -1;
+            unsigned ewords = 0;
             for (int t = 0; t < m; ++t) {
                 const int r = cta_rows[c][ch.row0 + t];
                 const int o = sol_index(s, r);
-                put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
+                if (!unit) put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
-                put_i(sec.exp, t, export_id[r]);
+                if (export_id[r] >= 0) {  // consecutive ids inside the chunk (wave order)
+                    if (ebase < 0) ebase = export_id[r];
+                    unsigned mask;
+                    std::memcpy(&mask, b + sec.exp + 16 + 8 * (t / 32), 4);
+                    mask |= 1u << (t % 32);
+                    std::memcpy(b + sec.exp + 16 + 8 * (t / 32), &mask, 4);
+                    ++ewords;
+                }
             }
-            for (int t = m; t < mp; ++t) {  // padded rows: harmless values
-                put_d(sec.diag, t, 1.0);
-                put_i(sec.exp, t, -1);
+            put_i(sec.exp, 0, ebase < 0 ? 0 : ebase);
+            for (int q = 0, pre = 0; q < (mp + 31) / 32; ++q) {  // prefix counts per 32-row word
+                unsigned mask;
+                std::memcpy(&mask, b + sec.exp + 16 + 8 * q, 4);
+                std::memcpy(b + sec.exp + 16 + 8 * q + 4, &pre, 4);
+                pre += __builtin_popcount(mask);
             }
+            (void)ewords;
+            if (!unit)
+                for (int t = m; t < mp; ++t) put_d(sec.diag, t, 1.0);  // padded rows: harmless values
             std::memcpy(b + sec.val, val.data(), 8 * val.size());
             if ((flags & 9) == 0) {  // 16-bit ring slots (byte offset / 8 < 2^16 for R + 1 + H <= 2^16)
                 for (std::size_t k = 0; k < dep.size(); ++k) {

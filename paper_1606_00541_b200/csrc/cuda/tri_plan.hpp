@@ -86,15 +86,20 @@ LevelLayout build_levels(const TriSource& s);
 // section before the tail sits at an offset computable from mp alone:
 //   WaveHeader (48 B)  {m, mp, q0, flags}, {nhalo, halo list, tail, hq0}, {r0, 0, 0, 0}
 //   uint2 seg[G]         per warp of the group: (t0 | t1 << 16, 0)
-//   double diag[mp]
+//   double diag[mp]      (absent when every diagonal of the chunk is 1.0, flags&64:
+//                        x = num * 1.0, bitwise num / 1.0; the ILU(0) L factor)
 //   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep -> 0.0 slot)
 //   dep[W][mp]           fast chunks (no tail, no x re-reads, flags & 9 == 0):
 //                        uint16 slot s of the x-ring array (own row q mod R,
 //                        the 0.0 slot R, staged value R + 1 + pos mod H), padded
 //                        to 16 bytes; otherwise int32 d: d >= 0 byte offset 8 s,
 //                        d < 0: x[-d-1] (wave order)
-//   int exp[mp] (mailbox id or -1), (oidx[mp] if flags&2); row t's x goes to
-//   wave position r0 + t, so no per-row solution index is stored
+//   exports              int base, 3 pad; uint2 {mask, prefix}[ceil(mp/32)]: row t
+//                        is exported iff bit t%32 of mask[t/32] is set, to mailbox
+//                        base + prefix + popc(lower bits) (mailbox ids follow the
+//                        wave order, so a chunk's exported rows are consecutive);
+//   (oidx[mp] if flags&2); row t's x goes to wave position r0 + t, so no per-row
+//   solution index is stored
 //   if flags&1: int tptr[mp+1 -> mult of 4], double tval[ntail -> even], int tdep[ntail -> mult of 4]
 //   int halo[nhalo -> mult of 4]   export ids whose mailboxes this chunk stages,
 //                                  in (ELL slot, row) order of first use
@@ -151,7 +156,8 @@ struct WaveSections {
 
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
-    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0
+    int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0,
+                                   //        64 unit diagonal (no diag section, no division)
     int nhalo, halo, tptr, hq0;    // halo id list / tail offsets, halo ring position of the first staged value
     int r0, pad0, pad1, pad2;      // wave position of the chunk's first row (where its x values go)
 };
@@ -165,10 +171,10 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     const int mp = round_up(m, 4);
     int at = kWaveHeaderBytes;
     b.seg = at;   at += round_up(8 * nw, 16);
-    b.diag = at;  at += 8 * mp;
+    b.diag = at;  if (!(flags & 64)) at += 8 * mp;  // unit-diagonal chunks store no diagonal
     b.val = at;   at += 8 * mp * w;
     b.dep = at;   at += (flags & 9) == 0 ? round_up(2 * mp * w, 16) : 4 * mp * w;  // fast chunks: 16-bit ring slots
-    b.exp = at;   at += 4 * mp;
+    b.exp = at;   at += 16 + 8 * ((mp + 31) / 32);    // export base id + {mask, prefix} per 32 rows
     b.oidx = at;  if (flags & 2) at += 4 * mp;
     b.tptr = at;  if (flags & 1) at += 4 * round_up(mp + 1, 4);
     b.tval = at;  if (flags & 1) at += 8 * round_up(ntail, 2);
