@@ -25,6 +25,7 @@ Options options();
 struct TriMirror {
     std::mutex mu;
     hec_tri_t handle = nullptr;
+    const void* source = nullptr;  // data() of the arrays the handle was built from
     TriMirror() = default;
     TriMirror(const TriMirror&) = delete;
     TriMirror& operator=(const TriMirror&) = delete;
@@ -34,6 +35,7 @@ struct TriMirror {
 struct PrecondMirror {
     std::mutex mu;
     hec_precond_t handle = nullptr;
+    const void* source = nullptr;
     PrecondMirror() = default;
     PrecondMirror(const PrecondMirror&) = delete;
     PrecondMirror& operator=(const PrecondMirror&) = delete;

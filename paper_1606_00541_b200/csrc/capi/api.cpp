@@ -149,18 +149,30 @@ hec_precond* build_precond(const BlockPreconditioner& m) {
 
 }  // namespace
 
+// The device mirror is built on first use and shared by copies of the object
+// (the reference's objects are immutable after construction, SPEC.md). A copy
+// owns separate arrays: it is recognised by their addresses and gets a device
+// copy of its own instead of the original's (returns nullptr: build one-off).
 hec_tri_t device_handle(const PreparedTriangular& p) {
     if (!p.device) throw std::invalid_argument("solve: PreparedTriangular has no device slot (use prepare_*)");
     std::lock_guard<std::mutex> g(p.device->mu);
-    if (!p.device->handle) p.device->handle = build_tri(p);
-    return p.device->handle;
+    const void* src = p.hec.csr.values.data();
+    if (!p.device->handle) {
+        p.device->handle = build_tri(p);
+        p.device->source = src;
+    }
+    return p.device->source == src ? p.device->handle : nullptr;
 }
 
 hec_precond_t device_handle(const BlockPreconditioner& m) {
     if (!m.device) throw std::invalid_argument("apply: BlockPreconditioner has no device slot");
     std::lock_guard<std::mutex> g(m.device->mu);
-    if (!m.device->handle) m.device->handle = build_precond(m);
-    return m.device->handle;
+    const void* src = m.prepared_l.hec.csr.values.data();
+    if (!m.device->handle) {
+        m.device->handle = build_precond(m);
+        m.device->source = src;
+    }
+    return m.device->source == src ? m.device->handle : nullptr;
 }
 
 // ------------------------------------------------------ drop-in C++ API ----
@@ -168,9 +180,9 @@ std::vector<double> solve(const PreparedTriangular& p, const std::vector<double>
     if (static_cast<int>(b.size()) != p.n) throw std::invalid_argument("solve: dimension mismatch");
     std::vector<double> x(p.n);
     if (p.n == 0) return x;
-    if (p.device) {
-        device_handle(p)->impl->solve_host(b.data(), x.data());
-    } else {  // hand-assembled object: build a one-off device copy
+    if (hec_tri_t h = p.device ? device_handle(p) : nullptr) {
+        h->impl->solve_host(b.data(), x.data());
+    } else {  // hand-assembled object or a copy: build a one-off device copy
         std::unique_ptr<hec_tri> t(build_tri(p));
         t->impl->solve_host(b.data(), x.data());
     }
@@ -181,9 +193,9 @@ std::vector<double> apply(const BlockPreconditioner& m, const std::vector<double
     if (static_cast<int>(r.size()) != m.n) throw std::invalid_argument("apply: dimension mismatch");
     std::vector<double> x(m.n);
     if (m.n == 0) return x;
-    if (m.device) {
-        device_handle(m)->impl->apply_host(r.data(), x.data());
-    } else {
+    if (hec_precond_t h = m.device ? device_handle(m) : nullptr) {
+        h->impl->apply_host(r.data(), x.data());
+    } else {  // hand-assembled object or a copy: one-off device copy
         std::unique_ptr<hec_precond> d(build_precond(m));
         d->impl->apply_host(r.data(), x.data());
     }
@@ -202,8 +214,8 @@ SolveResult gmres(const CsrMatrix& a, const std::vector<double>& b, const BlockP
     std::unique_ptr<hec_precond> tmp;
     dev::DevicePrecond* M = nullptr;
     if (m) {
-        if (m->device) {
-            M = device_handle(*m)->impl.get();
+        if (hec_precond_t h = m->device ? device_handle(*m) : nullptr) {
+            M = h->impl.get();
         } else {
             tmp.reset(build_precond(*m));
             M = tmp->impl.get();
@@ -865,6 +877,7 @@ int hec_prep_device(hec_prep_t h, hec_tri_t* t) {
     return guarded([&] {
         need(h, "hec_prep_device");
         *t = hec::device_handle(*h->p);
+        if (!*t) throw std::logic_error("hec_prep_device: device mirror belongs to another object");
     });
 }
 
@@ -942,6 +955,7 @@ int hec_bp_device(hec_bp_t m, hec_precond_t* d) {
     return guarded([&] {
         need(m, "hec_bp_device");
         *d = hec::device_handle(m->m);
+        if (!*d) throw std::logic_error("hec_bp_device: device mirror belongs to another object");
     });
 }
 

@@ -76,10 +76,24 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
                 throw std::invalid_argument("HEC_WAVE_G/K/RPL: no kernel for this solver shape");
         }
         if (const char* e = std::getenv("HEC_WAVE_SLABS")) cfg.pencils = std::atoi(e) == 0;  // layout knob
-        if (const char* e = std::getenv("HEC_WAVE_RING")) cfg.ring = std::atoi(e);           // x-ring entries (power of two)
-        if (const char* e = std::getenv("HEC_WAVE_INFLIGHT")) cfg.inflight = std::atoi(e);   // descriptor slots (power of two)
-        if (const char* e = std::getenv("HEC_WAVE_HALO_MAX")) cfg.halo_ring_max = std::atoi(e); // staged-halo ring cap
-        if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::atoi(e);       // spin back-off knob
+        auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+        if (const char* e = std::getenv("HEC_WAVE_RING")) {  // x-ring entries (power of two >= 1024)
+            cfg.ring = std::atoi(e);
+            if (!pow2(cfg.ring) || cfg.ring < 1024) throw std::invalid_argument("HEC_WAVE_RING: power of two >= 1024");
+        }
+        if (const char* e = std::getenv("HEC_WAVE_INFLIGHT")) {  // descriptor slots (power of two, 4..32)
+            cfg.inflight = std::atoi(e);
+            if (!pow2(cfg.inflight) || cfg.inflight < 4 || cfg.inflight > 32)
+                throw std::invalid_argument("HEC_WAVE_INFLIGHT: power of two in [4, 32]");
+        }
+        if (const char* e = std::getenv("HEC_WAVE_HALO_MAX")) {  // staged-halo ring cap (power of two)
+            cfg.halo_ring_max = std::atoi(e);
+            if (!pow2(cfg.halo_ring_max) || cfg.ring + 1 + cfg.halo_ring_max > 65536)
+                throw std::invalid_argument("HEC_WAVE_HALO_MAX: power of two with ring + 1 + halo <= 65536");
+        }
+        if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::max(0, std::atoi(e));  // poll back-off
+        if (const char* e = std::getenv("HEC_WAVE_WATCHDOG_MS"))
+            watchdog_ns_ = 1000000ULL * static_cast<unsigned long long>(std::max(1, std::atoi(e)));
         const int budget = smem_optin() - 1024;  // static shared + slack
         cfg.smem_bytes = budget;
         cfg.ctrl_bytes = kWaveCtrlBytes;
@@ -277,6 +291,7 @@ void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;
     a.spin_ns = spin_ns_;
+    a.watchdog_ns = watchdog_ns_;
     a.trace = trace;
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)

@@ -301,3 +301,39 @@ def test_wave_order_output(H, orc, strategy):
         torch.cuda.synchronize()
         assert bits_equal(x.cpu().numpy(), want)
         assert np.array_equal(np.sort(xw.cpu().numpy().view(np.uint64)), np.sort(want.view(np.uint64)))
+
+
+_WATCHDOG_CHILD = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_1606_00541_b200 as H
+n = 200000  # bidiagonal: 200000 levels, one row each -- a ~20-40 ms dependency chain
+a = H.csr_from_triples(n, n, [(i, i, 2.0) for i in range(n)] + [(i, i - 1, -1.0) for i in range(1, n)])
+t = H.DeviceTri.create(H.prepare_lower(a), strategy=2)
+b = torch.ones(n, dtype=torch.float64, device="cuda")
+x = torch.empty_like(b)
+try:
+    t.solve(b, x)
+    torch.cuda.synchronize()
+    print("SOLVED", float(x[-1].item()))
+except Exception as e:
+    print("ERROR", type(e).__name__, str(e)[:200])
+"""
+
+
+def test_watchdog_turns_a_stall_into_an_error():
+    # every wait in k_wave is bounded (HEC_WAVE_WATCHDOG_MS): with a 1 ms deadline the
+    # 200000-level chain cannot finish, the kernel traps and the call fails instead of
+    # hanging; with the default deadline the same solve completes
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _WATCHDOG_CHILD.format(root=root)
+    env = dict(os.environ, HEC_WAVE_WATCHDOG_MS="1")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert "ERROR" in p.stdout, p.stdout + p.stderr[-2000:]
+    env.pop("HEC_WAVE_WATCHDOG_MS")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert "SOLVED" in p.stdout, p.stdout + p.stderr[-2000:]
