@@ -31,6 +31,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "comm.hpp"
@@ -53,7 +55,7 @@ __device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int w
                                            unsigned* counter, double* out) {
     __shared__ double sw[kMaxOut][kT / 32];
     __shared__ bool last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;  // blockDim <= kT
     const int cnt = kc + (with_norm ? 1 : 0);
 #pragma unroll
     for (int k = 0; k < kMaxOut; ++k) {
@@ -67,8 +69,7 @@ __device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int w
     __syncthreads();
     if (threadIdx.x < cnt) {
         double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < kT / 32; ++q) s = __dadd_rn(s, sw[threadIdx.x][q]);
+        for (int q = 0; q < nwarps; ++q) s = __dadd_rn(s, sw[threadIdx.x][q]);
         partials[static_cast<size_t>(threadIdx.x) * gridDim.x + blockIdx.x] = s;
     }
     __threadfence();
@@ -77,7 +78,7 @@ __device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int w
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int k = warp; k < cnt; k += kT / 32) {  // one warp per output, fixed order
+    for (int k = warp; k < cnt; k += nwarps) {  // one warp per output, fixed order
         double s = 0.0;
         for (unsigned b = lane; b < gridDim.x; b += 32)
             s = __dadd_rn(s, __ldcg(&partials[static_cast<size_t>(k) * gridDim.x + b]));
@@ -97,7 +98,7 @@ __device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int w
 //            sqrt(max(0, c[kc] - sum_k c_k^2)) written to *s_out)
 //   out[k] = V_k . u (k < kc), out[kc] = u . u   if dots (u = w_out, or w_in
 //            when nothing is written; the norm only if with_norm)
-constexpr int kTile = 256;  // rows per tile = threads per block
+constexpr int kTile = 256;  // rows per tile = threads per block (at most; 128 for wide passes)
 struct MvArgs {
     int n, kc;
     size_t ldv;
@@ -118,14 +119,15 @@ struct MvArgs {
 // tile's byte count, then every lane issues the bulk copies of its columns (a
 // single thread issuing ~30 copies back to back would pace the stream).
 __device__ __forceinline__ void mv_issue(const MvArgs& a, int tile, double* stage, uint64_t* bar, int lane) {
-    const int r0 = tile * kTile;
-    const int m = min(kTile, a.n - r0);
+    const int rows = blockDim.x;
+    const int r0 = tile * rows;
+    const int m = min(rows, a.n - r0);
     const uint32_t bytes = static_cast<uint32_t>(((m + 1) & ~1) * 8);  // 16-byte multiple (columns are padded)
     const int nw = a.w_in ? 1 : 0;
     if (lane == 0) mbar_expect_tx(bar, bytes * static_cast<uint32_t>(a.kc + nw));
     __syncwarp();
     for (int k = lane; k < a.kc + nw; k += 32)
-        bulk_g2s(stage + k * kTile, k < a.kc ? a.V + k * a.ldv + r0 : a.w_in + r0, bytes, bar);
+        bulk_g2s(stage + k * rows, k < a.kc ? a.V + k * a.ldv + r0 : a.w_in + r0, bytes, bar);
 }
 
 __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
@@ -133,9 +135,9 @@ __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
     __shared__ uint64_t bar[2];
     __shared__ double sc[kMaxOut];
     __shared__ double s_scale;
-    const int tid = threadIdx.x;
-    const int ntiles = (a.n + kTile - 1) / kTile;
-    const int per_stage = (a.kc + 1) * kTile;
+    const int tid = threadIdx.x, rows = blockDim.x;
+    const int ntiles = (a.n + rows - 1) / rows;
+    const int per_stage = (a.kc + 1) * rows;
     if (tid < a.kc && a.c) sc[tid] = a.c[tid];
     if (tid == 0) {
         double s = 1.0;
@@ -166,20 +168,20 @@ __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
         const int q = it & 1;
         const double* st = mv_smem + q * per_stage;
         mbar_wait(&bar[q], (it >> 1) & 1);
-        const int i = tile * kTile + tid;
+        const int i = tile * rows + tid;
         if (i < a.n) {
-            double u = a.w_in ? st[a.kc * kTile + tid] : 0.0;
+            double u = a.w_in ? st[a.kc * rows + tid] : 0.0;
             if (a.w_out) {
 #pragma unroll
                 for (int k = 0; k < kKG; ++k)
-                    if (k < a.kc) u = __dsub_rn(u, __dmul_rn(sc[k], st[k * kTile + tid]));
+                    if (k < a.kc) u = __dsub_rn(u, __dmul_rn(sc[k], st[k * rows + tid]));
                 if (a.scale_mode) u = __ddiv_rn(u, s);
                 a.w_out[i] = u;
             }
             if (a.dots) {
 #pragma unroll
                 for (int k = 0; k < kKG; ++k)
-                    if (k < a.kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(st[k * kTile + tid], u));
+                    if (k < a.kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(st[k * rows + tid], u));
                 acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(u, u));
             }
         }
@@ -225,8 +227,48 @@ void halo_exchange(const DistSystem& S, double* vloc, double* sendbuf, cudaStrea
     S.comm->exchange(sendbuf, S.send_off, vloc + S.n_own, S.recv_off, st);
 }
 
+namespace {
+// HEC_GMRES_PROFILE=1: CUDA-event times of the phases of every inner iteration
+// (apply + SpMV with its exchanges, CGS2 pass 1, pass 2, normalisation), summed
+// and printed to stderr at the end of the solve (diagnostics; adds event syncs).
+struct PhaseProfile {
+    bool on = std::getenv("HEC_GMRES_PROFILE") != nullptr;
+    cudaEvent_t ev[5] = {};
+    bool marked[5] = {};
+    double ms[4] = {};
+    int iters = 0;
+    PhaseProfile() {
+        if (on)
+            for (auto& e : ev) cudaEventCreate(&e);
+    }
+    ~PhaseProfile() {
+        if (!on) return;
+        std::fprintf(stderr, "[hec gmres] %d iterations, ms per iteration: apply+spmv %.3f  pass1 %.3f  pass2 %.3f  "
+                             "normalise %.3f\n", iters, ms[0] / std::max(iters, 1), ms[1] / std::max(iters, 1),
+                     ms[2] / std::max(iters, 1), ms[3] / std::max(iters, 1));
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    void mark(cudaStream_t st, int k) {
+        if (!on) return;
+        cudaEventRecord(ev[k], st);
+        marked[k] = true;
+    }
+    void collect() {
+        if (!on || !marked[4]) return;
+        for (int k = 0; k < 4; ++k) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+            ms[k] += t;
+        }
+        ++iters;
+        for (bool& m : marked) m = false;
+    }
+};
+}  // namespace
+
 GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const GmresParams& cfg,
                         cudaStream_t st) {
+    PhaseProfile prof;
     if (cfg.restart < 1) throw std::invalid_argument("gmres: restart must be >= 1");
     if (cfg.max_iters < 0) throw std::invalid_argument("gmres: max_iters must be >= 0");
     if (cfg.rel_tol < 0.0 || cfg.abs_tol < 0.0) throw std::invalid_argument("gmres: tolerances must be >= 0");
@@ -247,7 +289,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
 
     DevBuf<double> V(static_cast<size_t>(mr + 1) * ldv), w(ldv), zloc(ldv), xloc(ldv), xc(ldv), r(ldv), b(ldv);
     DevBuf<double> hb(2 * static_cast<size_t>(mr) + 8), yv(static_cast<size_t>(mr) + 1);
-    DevBuf<double> partials(static_cast<size_t>(kMaxOut) * 8 * sms), sendbuf(std::max(S.n_send, 1));
+    DevBuf<double> partials(static_cast<size_t>(kMaxOut) * 16 * sms), sendbuf(std::max(S.n_send, 1));
     DevBuf<unsigned> counter(1);
     HEC_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), st));
     HEC_CUDA(cudaMemsetAsync(xloc.p, 0, sizeof(double) * ldv, st));
@@ -298,11 +340,14 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         m.partials = partials.p;
         m.counter = counter.p;
         m.out = outp;
-        const int smem = 2 * (kc + 1) * kTile * static_cast<int>(sizeof(double));
-        const int per_sm = std::max(1, std::min(8, (227 * 1024) / (smem + 2048)));
-        const int ntiles = (n + kTile - 1) / kTile;
+        // tiles of 256 rows, 128 when the pass is wide: at least three blocks (six
+        // tiles in flight) per SM
+        const int rows = (kc + 1) * kTile * 16 <= 72 * 1024 ? kTile : kTile / 2;
+        const int smem = 2 * (kc + 1) * rows * static_cast<int>(sizeof(double));
+        const int per_sm = std::max(1, std::min(2048 / rows, (227 * 1024) / (smem + 2048)));
+        const int ntiles = (n + rows - 1) / rows;
         const int g = std::max(1, std::min(ntiles, per_sm * sms));
-        k_mv<<<g, kTile, smem, st>>>(m);
+        k_mv<<<g, rows, smem, st>>>(m);
         HEC_CUDA(cudaGetLastError());
         ++out.launches;
     };
@@ -337,17 +382,22 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         bool lucky = false;
         while (j < mr && out.iterations < cfg.max_iters) {
             double* vj = V.p + j * ldv;
+            prof.mark(st, 0);
             apply_op(vj, w.p);
+            prof.mark(st, 1);
             const int kc = j + 1;
             if (kc <= kKG) {
                 // CGS2 pass 1: h1 = V^T w
                 mv(kc, V.p, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 0, hb1);
+                prof.mark(st, 2);
                 comm.allreduce_sum(hb1, kc, st);
                 // pass 2: w' = w - V h1; h2 = V^T w', ||w'||^2
                 mv(kc, V.p, hb1, w.p, w.p, 0, 1.0, nullptr, 1, 1, hb2);
+                prof.mark(st, 3);
                 comm.allreduce_sum(hb2, kc + 1, st);
                 // v_{j+1} = (w' - V h2) / ||w''||
                 mv(kc, V.p, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
+                prof.mark(st, 4);
             } else {
                 // more basis vectors than one fused pass holds: modified Gram-Schmidt,
                 // one vector at a time (each step still one dot + one all-reduce)
@@ -362,6 +412,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
             }
             HEC_CUDA(cudaMemcpyAsync(hh.data(), hb.p, sizeof(double) * (2 * mr + 8), cudaMemcpyDeviceToHost, st));
             HEC_CUDA(cudaStreamSynchronize(st));
+            prof.collect();
             for (int i = 0; i <= j; ++i) h[i + j * (mr + 1)] = hh[i] + hh[mr + 2 + i];
             const double hjj1 = hh[mr + 2 + kc + 1];
             h[(j + 1) + j * (mr + 1)] = hjj1;
