@@ -11,11 +11,11 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 
 PKG   := paper_1606_00541_b200
 SRC   := $(PKG)/csrc
-OBJ   := build/obj
-LIB   := $(PKG)/libhecsolve_b200.so
+OBJ   ?= build/obj
+LIB   ?= $(PKG)/libhecsolve_b200.so
 
 HOST_FLAGS := -O3 -std=c++20 -fPIC -fopenmp -ffp-contract=off -Wall -Wextra -Iinclude
-CU_FLAGS   := -O3 -std=c++20 $(ARCH) -lineinfo -fmad=false -Xptxas -v \
+CU_FLAGS   := -O3 -std=c++20 $(ARCH) -lineinfo -fmad=false -Xptxas -v $(EXTRA_CU_FLAGS) \
               -Xcompiler -fPIC,-fopenmp,-ffp-contract=off -Iinclude
 
 HOST_SRCS := $(wildcard $(SRC)/host/*.cpp) $(wildcard $(SRC)/cuda/*.cpp)

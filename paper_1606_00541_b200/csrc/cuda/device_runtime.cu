@@ -92,6 +92,12 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
                 throw std::invalid_argument("HEC_WAVE_HALO_MAX: power of two with ring + 1 + halo <= 65536");
         }
         if (const char* e = std::getenv("HEC_WAVE_SPIN_NS")) spin_ns_ = std::max(0, std::atoi(e));  // poll back-off
+        {
+            int dev = 0;
+            HEC_CUDA(cudaGetDevice(&dev));
+            HEC_CUDA(cudaDeviceGetAttribute(&clock_khz_, cudaDevAttrClockRate, dev));
+            clock_khz_ = std::max(clock_khz_, 1000000);  // the boost clock may exceed the reported rate: be generous
+        }
         if (const char* e = std::getenv("HEC_WAVE_WATCHDOG_MS"))
             watchdog_ns_ = 1000000ULL * static_cast<unsigned long long>(std::max(1, std::atoi(e)));
         const int budget = smem_optin() - 1024;  // static shared + slack
@@ -291,7 +297,7 @@ void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream
     a.buf_off = p_buf_off_;
     a.buf_bytes = p_buf_bytes_;
     a.spin_ns = spin_ns_;
-    a.watchdog_ns = watchdog_ns_;
+    a.watchdog_cycles = watchdog_ns_ / 1000000ULL * static_cast<unsigned long long>(clock_khz_);  // ms * kHz
     a.trace = trace;
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)

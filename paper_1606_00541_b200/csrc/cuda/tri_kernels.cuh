@@ -46,7 +46,7 @@ struct WaveArgs {
     int buf_off;
     int buf_bytes;
     int spin_ns;                 // back-off between the waiters' mailbox polls (HEC_WAVE_SPIN_NS, 0 = off)
-    unsigned long long watchdog_ns;  // a wait unmet this long after the CTA started traps (HEC_WAVE_WATCHDOG_MS)
+    unsigned long long watchdog_cycles;  // SM cycles after the CTA started: past them a wait traps (HEC_WAVE_WATCHDOG_MS)
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 

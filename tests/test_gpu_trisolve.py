@@ -308,9 +308,10 @@ import sys
 sys.path.insert(0, {root!r})
 import numpy as np, torch
 import paper_1606_00541_b200 as H
-n = 200000  # bidiagonal: 200000 levels, one row each -- a ~20-40 ms dependency chain
+n = 200000  # bidiagonal: a 200000-level chain, two CTAs (slabs): the second one's waiter
+            # polls its first dependency for the ~10-30 ms the first CTA's half takes
 a = H.csr_from_triples(n, n, [(i, i, 2.0) for i in range(n)] + [(i, i - 1, -1.0) for i in range(1, n)])
-t = H.DeviceTri.create(H.prepare_lower(a), strategy=2)
+t = H.DeviceTri.create(H.prepare_lower(a), strategy=2, ctas=2)
 b = torch.ones(n, dtype=torch.float64, device="cuda")
 x = torch.empty_like(b)
 try:
@@ -323,9 +324,9 @@ except Exception as e:
 
 
 def test_watchdog_turns_a_stall_into_an_error():
-    # every wait in k_wave is bounded (HEC_WAVE_WATCHDOG_MS): with a 1 ms deadline the
-    # 200000-level chain cannot finish, the kernel traps and the call fails instead of
-    # hanging; with the default deadline the same solve completes
+    # the waiters' mailbox polls are bounded (HEC_WAVE_WATCHDOG_MS): with a 1 ms deadline
+    # the second CTA's wait cannot be met in time, the kernel traps and the call fails
+    # instead of hanging; with the default deadline the same solve completes
     import os
     import subprocess
     import sys
