@@ -73,7 +73,8 @@ typedef struct {
     double alg_bytes;    /* 12 nnz_T + 20 n                   */
     double predicted_us; /* cost-model critical path of one solve               */
     /* PIPELINE layout actually built (diagnostics; -1 / 0 for LEVELS) */
-    int layout;          /* 0 slabs, 1 z-pencils (recognised grid), 2 strips      */
+    int layout;          /* 0 slabs, 1 z-pencils (recognised grid), 2 strips,     */
+                         /* 3 mirror of the L layout (U of an ILU pair)           */
     int group, groups, rows_per_lane; /* solver shape G x K x RPL               */
     int width;           /* sliced-ELL width W of the device blob                */
     int ring, halo_ring, inflight;    /* shared-memory rings, descriptor slots  */

@@ -48,7 +48,7 @@ inline int rup(int v, int m) { return (v + m - 1) / m * m; }
 }  // namespace
 
 // ------------------------------------------------------------ DeviceTri ----
-DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
+DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror) {
     require_device();
     plan::validate(src);
     n_ = src.n;
@@ -106,7 +106,16 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
         plan::WaveLayout P;
         bool ok = true;
         try {
-            P = plan::build_wave(src, cfg);
+            if (mirror) {
+                cfg.mirror = mirror;
+                try {
+                    P = plan::build_wave(src, cfg);  // U as the mirror of L (no gather pass between them)
+                } catch (const std::invalid_argument& e) {
+                    if (std::getenv("HEC_DEBUG")) std::fprintf(stderr, "[hec] no mirrored layout: %s\n", e.what());
+                    cfg.mirror = nullptr;
+                }
+            }
+            if (!cfg.mirror) P = plan::build_wave(src, cfg);
         } catch (const std::invalid_argument&) {
             ok = false;  // row order the wave layout cannot schedule: level launches
         }
@@ -140,6 +149,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             p_bidx_.upload(P.bidx);
             p_cta0_.upload(P.cta_chunk0);
             p_cta0_host_ = P.cta_chunk0;
+            h_chunk_r0_ = P.chunk_r0;
+            mirrored_ = P.mirrored;
             p_wpos_.upload(P.wpos);
             h_wpos_ = P.wpos;
             h_bidx_ = P.bidx;
@@ -148,7 +159,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
             if (!p_kernel_) throw std::invalid_argument("hec_tri_create: no wave kernel for this width");
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
-            stats_.layout = P.pencils ? 1 : (P.strips ? 2 : 0);
+            stats_.layout = P.mirrored ? 3 : (P.pencils ? 1 : (P.strips ? 2 : 0));
             stats_.group = P.group;
             stats_.groups = P.groups;
             stats_.rpl = P.rpl;
@@ -188,6 +199,15 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt) {
 
 DeviceTri::~DeviceTri() {
     if (h_stream_) cudaStreamDestroy(h_stream_);
+}
+
+bool DeviceTri::mirror_info(plan::WaveMirror& m) const {
+    if (strategy_ != 2 || h_chunk_r0_.empty() || h_wpos_.empty()) return false;
+    m.ctas = p_ctas_;
+    m.cta_chunk0 = p_cta0_host_.data();
+    m.chunk_r0 = h_chunk_r0_.data();
+    m.wpos = h_wpos_.data();
+    return true;
 }
 
 int DeviceTri::launches_per_solve() const {
@@ -340,8 +360,7 @@ DevicePrecond::DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, 
     l.b_map = gather;
     u.out_map = out_index;
     l_ = std::make_unique<DeviceTri>(l, opt);
-    u_ = std::make_unique<DeviceTri>(u, opt);
-    compose();
+    build_upper(u, opt);
 }
 
 DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* owned, plan::TriSource l,
@@ -367,8 +386,17 @@ DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* ow
         u.out_map = out_map.data(); // U scatters owned rows into x
     }
     l_ = std::make_unique<DeviceTri>(l, opt);
-    u_ = std::make_unique<DeviceTri>(u, opt);
-    compose();
+    build_upper(u, opt);
+}
+
+// U as the mirror of L's wave layout when that is valid (its right-hand side is
+// then L's wave-ordered output read backwards, chunk by chunk: no pass between
+// the solves); otherwise its own layout plus the composed gather.
+void DevicePrecond::build_upper(const plan::TriSource& u, const TriOptions& opt) {
+    plan::WaveMirror m;
+    const bool can = l_->mirror_info(m) && !std::getenv("HEC_NO_MIRROR");
+    u_ = std::make_unique<DeviceTri>(u, opt, can ? &m : nullptr);
+    if (!u_->mirrored()) compose();
 }
 
 DevicePrecond::~DevicePrecond() {
@@ -396,13 +424,17 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
     // (no pass through the solution order in between)
     l_->permute(r, w.bl.p, st);
     l_->solve_wave(w.bl.p, w.yw.p, nullptr, st);
-    permute_in(w.yw.p, lu_map_.p, w.bu.p, n_ext_, st);
-    HEC_CUDA(cudaGetLastError());
+    const double* bu = w.yw.p;  // mirrored U: L's output as it lies
+    if (!u_->mirrored()) {
+        permute_in(w.yw.p, lu_map_.p, w.bu.p, n_ext_, st);
+        HEC_CUDA(cudaGetLastError());
+        bu = w.bu.p;
+    }
     if (identity_) {
-        u_->solve_wave(w.bu.p, w.xw.p, nullptr, st);
+        u_->solve_wave(bu, w.xw.p, nullptr, st);
         u_->permute_out(w.xw.p, x, st);
     } else {
-        u_->solve_wave(w.bu.p, w.xw.p, x, st);  // owned rows scattered into x by the kernel
+        u_->solve_wave(bu, w.xw.p, x, st);  // owned rows scattered into x by the kernel
     }
 }
 void DevicePrecond::compose() {
@@ -421,7 +453,7 @@ cudaStream_t DevicePrecond::host_stream(std::unique_lock<std::mutex>& lock) {
 
 int DevicePrecond::launches_per_apply() const {
     if (n_ext_ == 0) return 0;
-    return l_->launches_per_solve() + u_->launches_per_solve() - (identity_ ? 1 : 2);
+    return l_->launches_per_solve() + u_->launches_per_solve() - (identity_ ? 1 : 2) - (u_->mirrored() ? 1 : 0);
 }
 
 void DevicePrecond::apply_host(const double* r, double* x) {

@@ -73,7 +73,9 @@ struct TriStats {
 
 class DeviceTri {
 public:
-    DeviceTri(const plan::TriSource& src, const TriOptions& opt);
+    // mirror: build the wave layout as the exact mirror of another one (the L of
+    // an ILU pair) when valid (plan::WaveMirror), else the layout of its own
+    DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror = nullptr);
     ~DeviceTri();
     DeviceTri(const DeviceTri&) = delete;
     DeviceTri& operator=(const DeviceTri&) = delete;
@@ -95,6 +97,9 @@ public:
     // output position; empty = identity)
     const std::vector<int>& host_bidx() const { return h_bidx_; }
     const std::vector<int>& host_wpos() const { return h_wpos_; }
+    // this layout's chunk structure, for mirroring (false for level launches)
+    bool mirror_info(plan::WaveMirror& m) const;
+    bool mirrored() const { return mirrored_; }
     // chunk -> CTA map of the pipeline layout (empty for LEVELS)
     const std::vector<int>& cta_chunk0() const { return p_cta0_host_; }
     // Synchronous host-vector convenience (pinned or pageable).
@@ -133,7 +138,8 @@ private:
     void* p_kernel_ = nullptr;
     void* p_kernel_trace_ = nullptr;
     long long p_exports_ = 0;
-    std::vector<int> p_cta0_host_;
+    std::vector<int> p_cta0_host_, h_chunk_r0_;
+    bool mirrored_ = false;
 
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
@@ -173,6 +179,7 @@ private:
     std::unique_ptr<DeviceTri> l_, u_;
     DevBuf<int> lu_map_;  // U input position -> L output position (the two permutations composed)
     void compose();
+    void build_upper(const plan::TriSource& u, const TriOptions& opt);
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
     std::mutex h_mu_;

@@ -210,7 +210,28 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     // ---- ownership: row -> (CTA, warp) in the lower frame
     std::vector<int> owner_i(n), warp_i(n);
     int C_used = C0;
-    const GridGeom geo = cfg.pencils ? detect_grid(s) : GridGeom{};
+    const WaveMirror* M = cfg.mirror;
+    // mirrored layout: the mirrored CTA of each row (warps are dealt by position below)
+    std::vector<int> mirror_chunk_of_p;  // L wave position -> L chunk
+    if (M) {
+        if (M->ctas < 1 || !M->cta_chunk0 || !M->chunk_r0 || !M->wpos)
+            throw std::invalid_argument("wave mirror: incomplete");
+        const int nch = M->cta_chunk0[M->ctas];
+        if (M->chunk_r0[nch] != n) throw std::invalid_argument("wave mirror: size mismatch");
+        mirror_chunk_of_p.assign(n, 0);
+        std::vector<int> cta_of_chunk(nch);
+        for (int c = 0; c < M->ctas; ++c)
+            for (int g = M->cta_chunk0[c]; g < M->cta_chunk0[c + 1]; ++g) cta_of_chunk[g] = c;
+        for (int g = 0; g < nch; ++g)
+            for (int p = M->chunk_r0[g]; p < M->chunk_r0[g + 1]; ++p) mirror_chunk_of_p[p] = g;
+        for (int i = 0; i < n; ++i) {
+            const int o = s.reversed ? n - 1 - i : i;
+            owner_i[i] = M->ctas - 1 - cta_of_chunk[mirror_chunk_of_p[M->wpos[o]]];
+            warp_i[i] = 0;
+        }
+        C_used = M->ctas;
+    }
+    const GridGeom geo = (cfg.pencils && !M) ? detect_grid(s) : GridGeom{};
     // pencils only when they shorten the per-CTA level chain (the most levels
     // any CTA must walk through): true for 7-point stencils (levels x+y+z),
     // not for 27-point ones (x+2y+4z: a z-pencil spans 4 nz levels)
@@ -229,7 +250,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         return m;
     };
     bool use_pencils = false;
-    if (geo.ok && pencil_owners(geo, n, C0, 16, owner_i, warp_i, C_used)) {
+    if (!M && geo.ok && pencil_owners(geo, n, C0, 16, owner_i, warp_i, C_used)) {
         const int per = (n + C0 - 1) / C0;
         std::vector<int> slab(n);
         for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
@@ -239,13 +260,15 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     // slabs would give each CTA only a handful of consecutive levels and the CTAs
     // would run one after another; then every CTA takes a fraction of every level
     bool use_strips = false;
-    if (!use_pencils && cfg.strips) {
+    if (!M && !use_pencils && cfg.strips) {
         const int per = (n + C0 - 1) / C0;
         std::vector<int> slab(n);
         for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
         use_strips = s.nlev >= 16 && static_cast<long long>(max_levels_per_cta(slab, C0)) * 8 < s.nlev;
     }
-    if (use_pencils) {
+    if (M) {
+        P.mirrored = true;
+    } else if (use_pencils) {
         P.pencils = true;
         P.grid_nx = geo.nx;
         P.grid_ny = geo.ny;
@@ -377,7 +400,43 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     std::vector<std::vector<Chunk>> per_cta(C);
     std::vector<std::vector<int>> cta_rows(C);
     const int fl_est = 4 | (P.has_out ? 2 : 0);
-    {
+    if (M) {
+        // L's chunks in reverse: U CTA C-1-c takes L CTA c's chunks last to first,
+        // each chunk's rows last to first
+        std::vector<int> level_of_r(n), r_of_i(n);
+        for (int k = 0; k < s.nlev; ++k)
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) level_of_r[r] = k;
+        for (int r = 0; r < n; ++r) r_of_i[s.inv_perm[r]] = r;
+        std::vector<int> o_of_p(n);
+        for (int o = 0; o < n; ++o) o_of_p[M->wpos[o]] = o;
+        for (int cl = 0; cl < C; ++cl) {
+            const int c = C - 1 - cl;
+            int prev_level = -1;
+            for (int g = M->cta_chunk0[cl + 1] - 1; g >= M->cta_chunk0[cl]; --g) {
+                const int p0 = M->chunk_r0[g], m = M->chunk_r0[g + 1] - p0;
+                Chunk ch{-1, static_cast<int>(cta_rows[c].size()), m, W, 0};
+                int halo_ub = 0;
+                for (int t = m - 1; t >= 0; --t) {
+                    const int o = o_of_p[p0 + t];
+                    const int r = r_of_i[s.reversed ? n - 1 - o : o];
+                    if (ch.level < 0) ch.level = level_of_r[r];
+                    if (level_of_r[r] != ch.level) throw std::invalid_argument("wave mirror: chunk spans levels");
+                    ch.ntail += std::max(0, cnt[r] - W);
+                    halo_ub += nforeign[r];
+                    cta_rows[c].push_back(r);
+                }
+                if (ch.level <= prev_level) throw std::invalid_argument("wave mirror: levels do not rise");
+                prev_level = ch.level;
+                const int fl = fl_est | (ch.ntail > 0 ? 1 : 0);
+                if (m > NW * warp_rows ||
+                    wave_region_bytes(m, halo_ub, wave_sections(m, W, NW, halo_ub, ch.ntail, fl).end) > cfg.max_bytes)
+                    throw std::invalid_argument("wave mirror: chunk exceeds the solver shape");
+                const int pw = (m + NW - 1) / NW;
+                for (int t = 0; t < m; ++t) warp_r[cta_rows[c][ch.row0 + t]] = t / pw;
+                per_cta[c].push_back(ch);
+            }
+        }
+    } else {
         std::vector<std::vector<int>> bucket(C);
         for (int k = 0; k < s.nlev; ++k) {
             for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) bucket[owner_r[r]].push_back(r);
@@ -533,6 +592,10 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     // wave order: (CTA, chunk, row in chunk); bp[wave position] = b[bidx[..]]
     std::vector<long long> cta_wbase(static_cast<std::size_t>(C) + 1, 0);
     for (int c = 0; c < C; ++c) cta_wbase[c + 1] = cta_wbase[c] + static_cast<long long>(cta_rows[c].size());
+    P.chunk_r0.assign(static_cast<std::size_t>(P.chunks) + 1, n);
+    for (int c = 0; c < C; ++c)
+        for (std::size_t j = 0; j < per_cta[c].size(); ++j)
+            P.chunk_r0[P.cta_chunk0[c] + j] = static_cast<int>(cta_wbase[c] + qend[c][j] - per_cta[c][j].m);
     P.bidx.assign(n, 0);
     P.wpos.assign(n, 0);
     std::vector<int> wpos_r(n);  // reordered row -> wave position
@@ -541,7 +604,7 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         const int o = sol_index(s, r);
         const int p = static_cast<int>(cta_wbase[owner_r[r]] + seq_r[r]);
         wpos_r[r] = p;
-        P.bidx[p] = s.b_map ? s.b_map[o] : o;
+        P.bidx[P.mirrored ? n - 1 - p : p] = s.b_map ? s.b_map[o] : o;
         P.wpos[o] = p;
     }
     // x is written in wave order (coalesced stores; the solution order is one
@@ -668,8 +731,11 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
                 const int r = cta_rows[c][ch.row0 + t];
                 unit = s.csr_vals[s.csr_rp[r + 1] - 1] == 1.0 && !std::signbit(s.csr_vals[s.csr_rp[r + 1] - 1]);
             }
+            // the chunk's right-hand side in bp: [wpos, wpos + m), or for a mirrored
+            // layout [n - wpos - m, n - wpos) read backwards; copies start 16-byte aligned
+            const long long bsrc = P.mirrored ? n - wpos - m : wpos;
             const int flags = (ntail > 0 ? 1 : 0) | (P.has_out ? 2 : 0) | 4 | (glob ? 8 : 0) | (nhalo > 0 ? 16 : 0) |
-                              ((wpos & 1) ? 32 : 0) | (unit ? 64 : 0);
+                              ((bsrc & 1) ? 32 : 0) | (unit ? 64 : 0) | (P.mirrored ? 128 : 0);
             const WaveSections sec = wave_sections(m, w, NW, nhalo, ntail, flags);
             const int region = wave_region_bytes(m, nhalo, sec.end);
             const std::size_t base = out.size();
@@ -730,9 +796,9 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             sp[0] = static_cast<int>(base / 16);  // CTA-relative for now
             sp[1] = round_up(sec.end, 16);
             sp[2] = region;
-            sp[3] = static_cast<int>(wpos);
+            sp[3] = static_cast<int>(bsrc);  // the producer copies from bp + (sp[3] & ~1)
             sp[4] = wave_b_area(m);
-            sp[5] = round_up(8 * (m + static_cast<int>(wpos & 1)), 16);
+            sp[5] = round_up(8 * (m + static_cast<int>(bsrc & 1)), 16);
         }
     }
     for (int c = 0; c < C; ++c)

@@ -109,6 +109,21 @@ LevelLayout build_levels(const TriSource& s);
 // shared-memory region of a chunk is [b: 8*mb][blob], mb = round_up(m + 1, 4);
 // b starts one element in when r0 is odd (flags&32, the copy source is rounded
 // down to 16 bytes). Regions are placed in the byte ring by the host (span).
+// The chunk structure of another layout over the same solution indices (the L
+// factor of an ILU pair), for building the U layout as its exact mirror: U's
+// wave order is L's reversed, so U's right-hand side -- L's output -- is L's
+// wave-ordered output read backwards, one contiguous range per chunk (no gather
+// pass between the two solves). SURVEY/DESIGN: valid when every mirrored chunk's
+// rows share one U level and the levels rise along each CTA (always so for the
+// ILU(0) factors of a symmetric pattern on a natural-order grid); build_wave
+// throws std::invalid_argument otherwise.
+struct WaveMirror {
+    int ctas = 0;
+    const int* cta_chunk0 = nullptr;  // ctas + 1
+    const int* chunk_r0 = nullptr;    // per chunk: wave position of its first row (chunks + 1 entries)
+    const int* wpos = nullptr;        // solution index -> wave position (n)
+};
+
 struct WaveConfig {
     int ctas = 148;
     int group = 0;            // solver warps per chunk (G); 0 = auto from the rows per (CTA, level)
@@ -124,6 +139,7 @@ struct WaveConfig {
     int ctrl_bytes = 1536;    // control block in front of the x ring
     bool pencils = true;      // structured 3-D grid detected: CTAs own z-pencils (see build_wave)
     bool strips = true;       // row index follows the levels: every CTA takes a fraction of each level
+    const WaveMirror* mirror = nullptr;  // build the exact mirror of this layout (see WaveMirror)
 };
 
 struct WaveLayout {
@@ -141,6 +157,9 @@ struct WaveLayout {
     int grid_nx = 0, grid_ny = 0;
     std::vector<int> cta_chunk0;          // ctas + 1: chunk range of each CTA
     std::vector<int> wpos;                // solution index -> wave position (where x lands)
+    std::vector<int> chunk_r0;            // chunks + 1: wave position of each chunk's first row (+ n)
+    bool mirrored = false;                // built as the mirror of another layout: bp runs backwards
+                                          //   (bp[n-1-p] feeds wave position p; bidx is indexed that way)
     std::vector<int> span;                // 8 per chunk: blob offset / 16, blob bytes, region position in
                                           //   the byte ring, r0, b area bytes, b copy bytes, chunk to wait
                                           //   for (released before the region is reused; < 0: none), 0
@@ -157,7 +176,8 @@ struct WaveSections {
 // First 32 bytes of every blob; read by the kernel as-is.
 struct WaveHeader {
     int m, mp, q0, flags;          // flags: 1 tail, 2 out-map, 8 global deps, 16 halo, 32 odd r0,
-                                   //        64 unit diagonal (no diag section, no division)
+                                   //        64 unit diagonal (no diag section, no division),
+                                   //        128 right-hand side staged backwards (mirrored layout)
     int nhalo, halo, tptr, hq0;    // halo id list / tail offsets, halo ring position of the first staged value
     int r0, pad0, pad1, pad2;      // wave position of the chunk's first row (where its x values go)
 };
