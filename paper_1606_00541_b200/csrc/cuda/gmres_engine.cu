@@ -9,18 +9,16 @@
 //   w = A M^-1 v_j      halo exchange of v_j (RAS), local ILU apply (the
 //                       persistent k_wave triangular solves), halo exchange of
 //                       z, HEC SpMV of the owned rows
-//   orthogonalisation   classical Gram-Schmidt instead of the reference's
-//                       modified Gram-Schmidt (gmres.cpp:72-77): the j+1 dots of
-//                       a pass are one fused multi-vector kernel and ONE
-//                       all-reduce. Pass 1 gives h1 = V^T w and ||w||^2; when the
-//                       projection removed more than half of ||w||^2 a second
-//                       pass re-orthogonalises ("twice is enough", Kahan-Parlett:
-//                       h2 = V^T w', ||w'||^2), else h2 = 0. So an iteration costs
-//                       one or two all-reduces instead of j+2; h = h1 + h2 and
-//                       ||w''||^2 = ||w'||^2 - ||h2||^2 (V orthonormal). In exact
-//                       arithmetic this and MGS produce the same Hessenberg
-//                       matrix; rounding differs, so iteration counts are
-//                       compared within +-1.
+//   orthogonalisation   classical Gram-Schmidt with one re-orthogonalisation
+//                       (CGS2) instead of the reference's modified Gram-Schmidt
+//                       (gmres.cpp:72-77): the j+1 dots of a pass are one fused
+//                       multi-vector kernel and ONE all-reduce, so an iteration
+//                       costs two all-reduces (pass 1: V^T w; pass 2: V^T w' and
+//                       ||w'||^2) instead of j+2. h = h1 + h2 and
+//                       ||w''||^2 = ||w'||^2 - ||h2||^2 (V orthonormal).
+//                       In exact arithmetic CGS2 and MGS produce the same
+//                       Hessenberg matrix; rounding differs, so iteration counts
+//                       are compared within +-1.
 //   restart             x += M^-1 (V y), r = b - A x (fused residual SpMV).
 //
 // Dots are deterministic: per-thread sums in a fixed element order, fixed
@@ -239,7 +237,6 @@ struct PhaseProfile {
     bool marked[5] = {};
     double ms[4] = {};
     int iters = 0;
-    const long long* reorth = nullptr;
     PhaseProfile() {
         if (on)
             for (auto& e : ev) cudaEventCreate(&e);
@@ -249,7 +246,6 @@ struct PhaseProfile {
         std::fprintf(stderr, "[hec gmres] %d iterations, ms per iteration: apply+spmv %.3f  pass1 %.3f  pass2 %.3f  "
                              "normalise %.3f\n", iters, ms[0] / std::max(iters, 1), ms[1] / std::max(iters, 1),
                      ms[2] / std::max(iters, 1), ms[3] / std::max(iters, 1));
-        std::fprintf(stderr, "[hec gmres] re-orthogonalised iterations: %lld\n", reorth ? *reorth : -1LL);
         for (auto& e : ev) cudaEventDestroy(e);
     }
     void mark(cudaStream_t st, int k) {
@@ -272,9 +268,7 @@ struct PhaseProfile {
 
 GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const GmresParams& cfg,
                         cudaStream_t st) {
-    GmresOutcome out;
     PhaseProfile prof;
-    prof.reorth = &out.reorthogonalisations;
     if (cfg.restart < 1) throw std::invalid_argument("gmres: restart must be >= 1");
     if (cfg.max_iters < 0) throw std::invalid_argument("gmres: max_iters must be >= 0");
     if (cfg.rel_tol < 0.0 || cfg.abs_tol < 0.0) throw std::invalid_argument("gmres: tolerances must be >= 0");
@@ -288,6 +282,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     const auto t0 = std::chrono::steady_clock::now();
     const int n = S.n_own;
     const int mr = cfg.restart;
+    GmresOutcome out;
     const int grid = std::max(1, std::min(4 * sm_count(), (n + kT - 1) / kT));
     const int sms = sm_count();
     const size_t ldv = static_cast<size_t>((std::max(S.n_loc, 1) + 31) / 32 * 32);  // 256-byte aligned columns
@@ -368,7 +363,6 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     const double bnorm = norm(b.p);
     const double threshold = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
     std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr), ny(mr + 1);
-    std::vector<double> h1h(static_cast<size_t>(mr) + 2);
     HEC_CUDA(cudaMemcpyAsync(r.p, b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     double rnorm = bnorm;
     bool stalled = false;
@@ -393,32 +387,16 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
             prof.mark(st, 1);
             const int kc = j + 1;
             if (kc <= kKG) {
-                // pass 1: h1 = V^T w and ||w||^2
-                mv(kc, V.p, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 1, hb1);
+                // CGS2 pass 1: h1 = V^T w
+                mv(kc, V.p, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 0, hb1);
                 prof.mark(st, 2);
-                comm.allreduce_sum(hb1, kc + 1, st);
-                // "twice is enough" (Kahan-Parlett): re-orthogonalise only when the
-                // projection removed more than half of ||w||^2, i.e. when w' is at risk
-                // of having lost its orthogonality to rounding
-                HEC_CUDA(cudaMemcpyAsync(h1h.data(), hb1, sizeof(double) * (kc + 1), cudaMemcpyDeviceToHost, st));
-                HEC_CUDA(cudaStreamSynchronize(st));
-                double hh1 = 0.0;
-                for (int i = 0; i < kc; ++i) hh1 += h1h[i] * h1h[i];
-                const double wp2 = h1h[kc] - hh1;
-                if (wp2 > 0.5 * h1h[kc]) {
-                    // v_{j+1} = (w - V h1) / sqrt(||w||^2 - ||h1||^2); h2 = 0
-                    HEC_CUDA(cudaMemsetAsync(hb2, 0, sizeof(double) * (kc + 1), st));
-                    prof.mark(st, 3);
-                    mv(kc, V.p, hb1, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
-                } else {
-                    ++out.reorthogonalisations;
-                    // pass 2: w' = w - V h1; h2 = V^T w', ||w'||^2
-                    mv(kc, V.p, hb1, w.p, w.p, 0, 1.0, nullptr, 1, 1, hb2);
-                    prof.mark(st, 3);
-                    comm.allreduce_sum(hb2, kc + 1, st);
-                    // v_{j+1} = (w' - V h2) / ||w''||
-                    mv(kc, V.p, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
-                }
+                comm.allreduce_sum(hb1, kc, st);
+                // pass 2: w' = w - V h1; h2 = V^T w', ||w'||^2
+                mv(kc, V.p, hb1, w.p, w.p, 0, 1.0, nullptr, 1, 1, hb2);
+                prof.mark(st, 3);
+                comm.allreduce_sum(hb2, kc + 1, st);
+                // v_{j+1} = (w' - V h2) / ||w''||
+                mv(kc, V.p, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
                 prof.mark(st, 4);
             } else {
                 // more basis vectors than one fused pass holds: modified Gram-Schmidt,

@@ -26,7 +26,6 @@ struct GmresOutcome {
     double solve_seconds = 0.0;
     long long launches = 0;
     long long allreduces = 0, exchanges = 0;
-    long long reorthogonalisations = 0;  // iterations that needed the second Gram-Schmidt pass
     std::vector<double> inner_residuals;
 };
 

@@ -1,7 +1,6 @@
 """TEST MODEL of the distributed GMRES engine (csrc/cuda/gmres_engine.cu) for the
 CPU suite: the same algorithm -- reference gmres.cpp:28-137 control flow and
-Givens arithmetic, classical Gram-Schmidt re-orthogonalised when "twice is
-enough" asks for it (one or two all-reduces per iteration),
+Givens arithmetic, CGS2 orthogonalisation with two all-reduces per iteration,
 halo exchanges before the local apply and the local SpMV -- in numpy, with the
 local work done by the C oracle and the collectives by a torch.distributed
 (gloo) group. It checks, on CPU with world sizes > 1, that the product's C++
@@ -105,23 +104,13 @@ def gmres(local, comm, plan, b_own, restart=20, max_iters=10000, rel_tol=1e-6, a
         j, lucky = 0, False
         while j < mr and iters < max_iters:
             w = op(V[j])
-            red = comm.allreduce(np.concatenate([V[:j + 1] @ w, [np.dot(w, w)]]))  # pass 1 + ||w||^2
-            h1, w2 = red[:j + 1], red[j + 1]
-            wp2 = w2 - float(np.dot(h1, h1))
-            if wp2 > 0.5 * w2:                                         # twice is enough: one pass
-                h2 = np.zeros(j + 1)
-                hjj1 = math.sqrt(max(wp2, 0.0))
-                base = w
-                coef = h1
-            else:                                                      # CGS2 pass 2
-                w = w - h1 @ V[:j + 1]
-                red = comm.allreduce(np.concatenate([V[:j + 1] @ w, [np.dot(w, w)]]))
-                h2, ww = red[:j + 1], red[j + 1]
-                hjj1 = math.sqrt(max(ww - float(np.dot(h2, h2)), 0.0))
-                base = w
-                coef = h2
+            h1 = comm.allreduce(V[:j + 1] @ w)                       # CGS2 pass 1
+            w = w - h1 @ V[:j + 1]
+            red = comm.allreduce(np.concatenate([V[:j + 1] @ w, [np.dot(w, w)]]))  # pass 2 + ||w'||^2
+            h2, ww = red[:j + 1], red[j + 1]
+            hjj1 = math.sqrt(max(ww - float(np.dot(h2, h2)), 0.0))
             if hjj1 > 1e-300:
-                V[j + 1] = (base - coef @ V[:j + 1]) / hjj1
+                V[j + 1] = (w - h2 @ V[:j + 1]) / hjj1
             else:
                 lucky = True
             h[:j + 1, j] = h1 + h2
