@@ -158,14 +158,16 @@ class RasSolver:
         if comm == "none":
             spec.kind = L.COMM_NONE
         elif comm == "nccl":
-            import torch
-            import torch.distributed as dist
             uid = (C.c_ubyte * 128)()
             if rank == 0:
                 check(lib.hec_nccl_unique_id(uid))
-            t = torch.tensor(bytearray(uid), dtype=torch.uint8, device="cuda")
-            dist.broadcast(t, 0)
-            self._uid = (C.c_ubyte * 128)(*t.cpu().tolist())
+            if world > 1:  # rank 0's id to every rank (torch.distributed is the bootstrap channel)
+                import torch
+                import torch.distributed as dist
+                t = torch.tensor(bytearray(uid), dtype=torch.uint8, device="cuda")
+                dist.broadcast(t, 0)
+                uid = (C.c_ubyte * 128)(*t.cpu().tolist())
+            self._uid = uid
             spec.kind = L.COMM_NCCL
             spec.nccl_id = C.cast(self._uid, C.POINTER(C.c_ubyte))
         elif comm == "callbacks":

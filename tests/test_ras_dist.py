@@ -210,3 +210,23 @@ def test_ras_device_multi_rank_one_gpu(ref, world):
         assert o["comm"] == "callbacks" and o["exchanges"] > 0
         # two all-reduces per iteration plus one per norm (CGS2), not j + 2
         assert o["allreduces"] <= 2 * o["iters"] + 2 * (o["iters"] // 30 + 2)
+
+
+@pytest.mark.gpu
+def test_ras_nccl_backend_one_rank(H, ref):
+    # the NCCL backend end to end on one rank: libnccl opened at run time (sharing the
+    # copy torch loaded), a one-rank communicator, every all-reduce of the engine through
+    # ncclAllReduce on the solve's stream; same iterations and apply as without comm
+    pytest.importorskip("torch")
+    from paper_1606_00541_b200 import _lib, ras
+    assert _lib.lib.hec_nccl_version() > 0
+    a = H.gen_poisson7(20, 18, 16)
+    A = Csr.of(a)
+    b = ref.spmv(A, np.ones(a.n_rows))
+    s1, s0 = ras.RasSolver(a, overlap=1, comm="nccl"), ras.RasSolver(a, overlap=1, comm="none")
+    x1, r1 = s1.gmres(b, restart=30)
+    x0, r0 = s0.gmres(b, restart=30)
+    assert r1.converged and r1.iterations == r0.iterations and r1.allreduces > 0 and r0.allreduces == 0
+    assert bits_equal(x1, x0)  # a one-rank sum changes nothing
+    r = np.random.default_rng(5).uniform(-1, 1, a.n_rows)
+    assert bits_equal(s1.apply_host(r), s0.apply_host(r))
