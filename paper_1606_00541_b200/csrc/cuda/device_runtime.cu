@@ -160,6 +160,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
             stats_.layout = P.mirrored ? 3 : (P.pencils ? 1 : (P.strips ? 2 : 0));
+            spare_ = make_workspace();
             stats_.group = P.group;
             stats_.groups = P.groups;
             stats_.rpl = P.rpl;
@@ -215,21 +216,48 @@ int DeviceTri::launches_per_solve() const {
     return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 3;  // permute-in + wave + permute-out
 }
 
+// Mailboxes, counters and scratch of the solves enqueued on one stream (so solves
+// on different streams may run concurrently). The handle is created with one
+// spare, which the first stream it is used on takes without allocating or
+// synchronising -- so a fresh stream may go straight into CUDA-graph capture.
+// Any further stream allocates (not allowed while that stream is capturing).
+std::unique_ptr<DeviceTri::Workspace> DeviceTri::make_workspace() const {
+    auto w = std::make_unique<Workspace>();
+    w->counters.alloc(3);  // ticket, CTAs finished, mailbox epoch (advanced by the kernel itself)
+    const uint32_t init[3] = {0u, 0u, 1u};
+    HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
+    w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
+    w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
+    w->xw.alloc(static_cast<std::size_t>(std::max(n_, 1)));
+    HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
+    HEC_CUDA(cudaDeviceSynchronize());
+    return w;
+}
+
 DeviceTri::Workspace& DeviceTri::workspace(cudaStream_t st) {
     std::lock_guard<std::mutex> g(mu_);
     auto& w = ws_[st];
     if (!w) {
-        w = std::make_unique<Workspace>();
-        w->counters.alloc(3);  // ticket, CTAs finished, mailbox epoch (advanced by the kernel itself)
-        const uint32_t init[3] = {0u, 0u, 1u};
-        HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
-        w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
-        w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
-        w->xw.alloc(static_cast<std::size_t>(std::max(n_, 1)));
-        HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
-        HEC_CUDA(cudaDeviceSynchronize());
+        if (spare_) {
+            w = std::move(spare_);
+        } else {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            HEC_CUDA(cudaStreamIsCapturing(st, &cs));
+            if (cs != cudaStreamCaptureStatusNone)
+                throw std::runtime_error("hec: first solve of this handle on a stream that is being captured; "
+                                         "run one solve on that stream before capturing");
+            w = make_workspace();
+        }
     }
     return *w;
+}
+
+void DeviceTri::release_workspace(cudaStream_t st) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = ws_.find(st);
+    if (it == ws_.end()) return;
+    if (!spare_) spare_ = std::move(it->second);  // keep one for the next stream
+    ws_.erase(it);
 }
 
 void DeviceTri::permute(const double* b, double* bp, cudaStream_t st) const {

@@ -106,6 +106,8 @@ public:
     void solve_host(const double* b, double* x);
     const TriStats& stats() const { return stats_; }
     int n() const { return n_; }
+    // drops the workspace of a stream the caller is about to destroy (kept as the spare)
+    void release_workspace(cudaStream_t st);
     int launches_per_solve() const;
 
 private:
@@ -116,6 +118,7 @@ private:
         DevBuf<double> xw;                    // solution in wave order
     };
     Workspace& workspace(cudaStream_t st);
+    std::unique_ptr<Workspace> make_workspace() const;
     void run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st);
 
     int n_ = 0;
@@ -143,6 +146,7 @@ private:
 
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;
+    std::unique_ptr<Workspace> spare_;  // taken by the first stream (no allocation, capture-safe)
     // host-call staging
     std::mutex h_mu_;
     DevBuf<double> h_b_, h_x_;

@@ -3,11 +3,11 @@
 
 namespace hec::dev {
 
- HEC_WAVE_INST(1) HEC_WAVE_INST(2) HEC_WAVE_INST(3)
-
 void* wave_kernel_a(int width, int group, int groups, int rpl, bool trace) {
     switch (width) {
-         HEC_PICK(1) HEC_PICK(2) HEC_PICK(3)
+        case 1: return wave_pick<1>(group, groups, rpl, trace);
+        case 2: return wave_pick<2>(group, groups, rpl, trace);
+        case 3: return wave_pick<3>(group, groups, rpl, trace);
         default: return nullptr;
     }
 }

@@ -3,11 +3,11 @@
 
 namespace hec::dev {
 
- HEC_WAVE_INST(4) HEC_WAVE_INST(5) HEC_WAVE_INST(6)
-
 void* wave_kernel_b(int width, int group, int groups, int rpl, bool trace) {
     switch (width) {
-         HEC_PICK(4) HEC_PICK(5) HEC_PICK(6)
+        case 4: return wave_pick<4>(group, groups, rpl, trace);
+        case 5: return wave_pick<5>(group, groups, rpl, trace);
+        case 6: return wave_pick<6>(group, groups, rpl, trace);
         default: return nullptr;
     }
 }

@@ -3,11 +3,11 @@
 
 namespace hec::dev {
 
- HEC_WAVE_INST(7) HEC_WAVE_INST(8) HEC_WAVE_INST(10)
-
 void* wave_kernel_c(int width, int group, int groups, int rpl, bool trace) {
     switch (width) {
-         HEC_PICK(7) HEC_PICK(8) HEC_PICK(10)
+        case 7: return wave_pick<7>(group, groups, rpl, trace);
+        case 8: return wave_pick<8>(group, groups, rpl, trace);
+        case 10: return wave_pick<10>(group, groups, rpl, trace);
         default: return nullptr;
     }
 }

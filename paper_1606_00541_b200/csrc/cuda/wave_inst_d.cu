@@ -3,11 +3,10 @@
 
 namespace hec::dev {
 
- HEC_WAVE_INST(13) HEC_WAVE_INST(16)
-
 void* wave_kernel_d(int width, int group, int groups, int rpl, bool trace) {
     switch (width) {
-         HEC_PICK(13) HEC_PICK(16)
+        case 13: return wave_pick<13>(group, groups, rpl, trace);
+        case 16: return wave_pick<16>(group, groups, rpl, trace);
         default: return nullptr;
     }
 }

@@ -259,6 +259,28 @@ def test_cuda_graph_replay(H, orc):
         assert bits_equal(x.cpu().numpy(), orc.solve(ou, orc.solve(ol, b))), rep
 
 
+def test_cuda_graph_capture_on_a_fresh_stream(H, orc):
+    # a new handle's first stream takes the preallocated workspace: capture works
+    # without a warm-up solve on that stream (no allocation, no synchronisation)
+    torch = pytest.importorskip("torch")
+    a = H.gen_poisson7(24, 22, 20)
+    f = H.ilu0(a)
+    tl = H.DeviceTri.create(H.prepare_lower(f.l), strategy=2)
+    ol = orc.prepare(to_oracle(f.l))
+    s = torch.cuda.Stream()
+    bd = torch.zeros(a.n_rows, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(bd)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        tl.solve(bd, y, stream=s)
+    b = np.random.default_rng(31).uniform(-1, 1, a.n_rows)
+    bd.copy_(torch.from_numpy(b))
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert bits_equal(y.cpu().numpy(), orc.solve(ol, b))
+
+
 def test_signed_zero_rhs(H, orc):
     # b = A * 1 leaves exact zeros in the interior (the bench right-hand side);
     # zero numerators take the kernel's a * RN(1/d) shortcut and must keep the
