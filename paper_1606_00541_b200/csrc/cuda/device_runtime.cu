@@ -194,6 +194,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
                  L.tail_dep.size()) +
             8 * (L.ell_val.size() + L.diag.size() + L.tail_val.size()));
         stats_.threads = 256;
+        spare_ = make_workspace();
     }
     stats_.strategy = strategy_;
 }
@@ -213,7 +214,8 @@ bool DeviceTri::mirror_info(plan::WaveMirror& m) const {
 
 int DeviceTri::launches_per_solve() const {
     if (n_ == 0) return 0;
-    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) - 1 : 3;  // permute-in + wave + permute-out
+    // levels: the argument kernel + one kernel per level (one graph launch); wave: permute-in + wave + permute-out
+    return strategy_ == 1 ? static_cast<int>(level_starts_.size()) : 3;
 }
 
 // Mailboxes, counters and scratch of the solves enqueued on one stream (so solves
@@ -223,6 +225,10 @@ int DeviceTri::launches_per_solve() const {
 // Any further stream allocates (not allowed while that stream is capturing).
 std::unique_ptr<DeviceTri::Workspace> DeviceTri::make_workspace() const {
     auto w = std::make_unique<Workspace>();
+    if (strategy_ == 1) {  // level launches: the argument block; the graph is captured on first use
+        w->largs.alloc(sizeof(LevelArgs));
+        return w;
+    }
     w->counters.alloc(3);  // ticket, CTAs finished, mailbox epoch (advanced by the kernel itself)
     const uint32_t init[3] = {0u, 0u, 1u};
     HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
@@ -304,8 +310,23 @@ void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* ou
         a.tail_val = l_tail_val_.p;
         a.width = l_width_;
         a.ld = l_ld_;
-        launch_levels(a, level_starts_.data(), static_cast<int>(level_starts_.size()) - 1, st);
+        Workspace& w = workspace(st);
+        LevelArgs* dev = reinterpret_cast<LevelArgs*>(w.largs.p);
+        const int nlev = static_cast<int>(level_starts_.size()) - 1;
+        if (!w.levels) {  // capture the level launches once, on a private stream
+            cudaStream_t cs = nullptr;
+            HEC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cudaGraph_t graph = nullptr;
+            HEC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            launch_levels(dev, level_starts_.data(), nlev, cs);
+            HEC_CUDA(cudaStreamEndCapture(cs, &graph));
+            HEC_CUDA(cudaGraphInstantiate(&w.levels, graph, 0));
+            cudaGraphDestroy(graph);
+            cudaStreamDestroy(cs);
+        }
+        set_level_args(a, dev, st);
         HEC_CUDA(cudaGetLastError());
+        HEC_CUDA(cudaGraphLaunch(w.levels, st));
     }
 }
 

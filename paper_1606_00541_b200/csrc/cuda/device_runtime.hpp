@@ -116,6 +116,12 @@ private:
         DevBuf<unsigned long long> mailbox;   // cross-CTA values, 2 epoch-tagged words each
         DevBuf<double> bp;                    // right-hand side in reordered-row order
         DevBuf<double> xw;                    // solution in wave order
+        // LEVELS: the argument block and the captured graph of the level launches
+        DevBuf<unsigned char> largs;
+        cudaGraphExec_t levels = nullptr;
+        ~Workspace() {
+            if (levels) cudaGraphExecDestroy(levels);
+        }
     };
     Workspace& workspace(cudaStream_t st);
     std::unique_ptr<Workspace> make_workspace() const;

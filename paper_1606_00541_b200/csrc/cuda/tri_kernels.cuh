@@ -50,7 +50,9 @@ struct WaveArgs {
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 
-void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st);
+// one launch per level, arguments read from dev_args (capturable once, replayed for any vectors)
+void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, int nlev, cudaStream_t st);
+void set_level_args(const LevelArgs& a, LevelArgs* dev, cudaStream_t st);
 // kernel for sliced-ELL width W (one of 1-8, 10, 13, 16) and solver shape
 // (group warps G x groups K x rpl rows per lane, see wave_inst.cuh); nullptr
 // when that combination is not instantiated

@@ -34,9 +34,14 @@ __device__ __forceinline__ double sub_prod(double acc, double v, double x) {
     return __dsub_rn(acc, __dmul_rn(v, x));
 }
 
-__global__ void k_level_rows(LevelArgs a, int r0, int r1) {
+// The level kernels of one solve read their argument block from device memory,
+// so the whole sequence of launches is captured once in a CUDA graph per stream
+// and replayed for any vectors: one argument-setting kernel + one graph launch
+// per solve instead of one launch per level.
+__global__ void k_level_rows(const LevelArgs* __restrict__ pa, int r0, int r1) {
     const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= r1) return;
+    const LevelArgs& a = *pa;
     double acc = a.b[a.b_ordered ? r : a.bidx[r]];
     for (int k = 0; k < a.width; ++k) {
         const size_t slot = static_cast<size_t>(k) * a.ld + r;
@@ -52,12 +57,18 @@ __global__ void k_level_rows(LevelArgs a, int r0, int r1) {
     }
 }
 
-void launch_levels(const LevelArgs& a, const int* level_starts_host, int nlev, cudaStream_t st) {
+__global__ void k_set_level_args(LevelArgs a, LevelArgs* dst) { *dst = a; }
+
+void set_level_args(const LevelArgs& a, LevelArgs* dev, cudaStream_t st) {
+    k_set_level_args<<<1, 1, 0, st>>>(a, dev);
+}
+
+void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, int nlev, cudaStream_t st) {
     for (int k = 0; k < nlev; ++k) {
         const int r0 = level_starts_host[k], r1 = level_starts_host[k + 1];
         const int m = r1 - r0;
         const int tpb = m >= 256 ? 256 : (m >= 128 ? 128 : 64);
-        k_level_rows<<<(m + tpb - 1) / tpb, tpb, 0, st>>>(a, r0, r1);
+        k_level_rows<<<(m + tpb - 1) / tpb, tpb, 0, st>>>(dev_args, r0, r1);
     }
 }
 
