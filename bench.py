@@ -480,17 +480,27 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        print(json.dumps(run_reference_arm(args)), flush=True)
+        line = run_reference_arm(args)
+        # the reference arm runs the reference library only: the product package must not be loaded
+        assert "paper_1606_00541_b200" not in sys.modules, "reference arm imported the product"
+        line["product_loaded"] = False
+        print(json.dumps(line), flush=True)
         return 0
 
     import torch
     import paper_1606_00541_b200 as H
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
-    device = torch.device("cuda", local)
+    device = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(device)
     if world > 1:
-        torch.distributed.init_process_group("nccl", device_id=device)
+        # HEC_BENCH_BACKEND=gloo: several ranks on one GPU (control-flow test; RAS then
+        # uses host-callback collectives instead of NCCL)
+        backend = os.environ.get("HEC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=device)
+        else:
+            torch.distributed.init_process_group(backend)
     with_cpu = rank == 0 and world == 1
     head = measure_config(H, torch, args.config, args, world, device, with_cpu)
     result = {"metric": head.pop("metric"), "value": head.pop("value"), "unit": head.pop("unit"), "n_gpus": world,
