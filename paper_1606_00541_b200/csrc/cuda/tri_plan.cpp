@@ -756,7 +756,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             for (int t = 0; t < m; ++t) {
                 const int r = cta_rows[c][ch.row0 + t];
                 const int o = sol_index(s, r);
-                if (!unit) put_d(sec.diag, t, s.csr_vals[s.csr_rp[r + 1] - 1]);
+                if (!unit) {
+                    // RN(1/d): IEEE division on the host is the correctly rounded
+                    // reciprocal __drcp_rn would give (the kernel uses it only while
+                    // |d| is inside the Markstein guard, where it is normal)
+                    const double d = s.csr_vals[s.csr_rp[r + 1] - 1];
+                    put_d(sec.diag, t, d);
+                    put_d(sec.diag + 8 * mp, t, 1.0 / d);
+                }
                 if (flags & 2) put_i(sec.oidx, t, s.out_map[o]);
                 if (export_id[r] >= 0) {  // consecutive ids inside the chunk (wave order)
                     if (ebase < 0) ebase = export_id[r];
@@ -776,7 +783,10 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
             }
             (void)ewords;
             if (!unit)
-                for (int t = m; t < mp; ++t) put_d(sec.diag, t, 1.0);  // padded rows: harmless values
+                for (int t = m; t < mp; ++t) {  // padded rows: harmless values
+                    put_d(sec.diag, t, 1.0);
+                    put_d(sec.diag + 8 * mp, t, 1.0);
+                }
             std::memcpy(b + sec.val, val.data(), 8 * val.size());
             if ((flags & 9) == 0) {  // 16-bit ring slots (byte offset / 8 < 2^16 for R + 1 + H <= 2^16)
                 for (std::size_t k = 0; k < dep.size(); ++k) {

@@ -86,8 +86,10 @@ LevelLayout build_levels(const TriSource& s);
 // section before the tail sits at an offset computable from mp alone:
 //   WaveHeader (48 B)  {m, mp, q0, flags}, {nhalo, halo list, tail, hq0}, {r0, 0, 0, 0}
 //   uint2 seg[G]         per warp of the group: (t0 | t1 << 16, 0)
-//   double diag[mp]      (absent when every diagonal of the chunk is 1.0, flags&64:
-//                        x = num * 1.0, bitwise num / 1.0; the ILU(0) L factor)
+//   double diag[mp], rcp[mp]  the diagonal and RN(1/diag), computed here once
+//                        instead of per solve (absent when every diagonal of the
+//                        chunk is 1.0, flags&64: x = num * 1.0, bitwise num / 1.0;
+//                        the ILU(0) L factor)
 //   double val[W][mp]    sliced ELL, slot-major (padding: value 0, dep -> 0.0 slot)
 //   dep[W][mp]           fast chunks (no tail, no x re-reads, flags & 9 == 0):
 //                        uint16 slot s of the x-ring array (own row q mod R,
@@ -191,7 +193,7 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
     const int mp = round_up(m, 4);
     int at = kWaveHeaderBytes;
     b.seg = at;   at += round_up(8 * nw, 16);
-    b.diag = at;  if (!(flags & 64)) at += 8 * mp;  // unit-diagonal chunks store no diagonal
+    b.diag = at;  if (!(flags & 64)) at += 16 * mp;  // diagonal + reciprocal; none when unit
     b.val = at;   at += 8 * mp * w;
     b.dep = at;   at += (flags & 9) == 0 ? round_up(2 * mp * w, 16) : 4 * mp * w;  // fast chunks: 16-bit ring slots
     b.exp = at;   at += 16 + 8 * ((mp + 31) / 32);    // export base id + {mask, prefix} per 32 rows

@@ -75,6 +75,41 @@ def main():
     per = [(done[c0[c + 1] - 1] - done[c0[c]]) / max(c0[c + 1] - c0[c] - 1, 1) for c in range(ncta)]
     print(f"per-CTA chunk period: p10 {np.percentile(per,10):.0f} p50 {np.percentile(per,50):.0f} "
           f"p90 {np.percentile(per,90):.0f} ns")
+    # chunk period (done_j - done_{j-1}) of chunks whose halo was staged before the
+    # previous chunk finished, by rows in the chunk: flat = latency chain, rising = throughput
+    rows = tr[:, 7]
+    per_rows = {}
+    for c in range(ncta):
+        for j in range(c0[c] + 1, c0[c + 1]):
+            if ready[j] <= done[j - 1]:
+                per_rows.setdefault(int(rows[j]) // 64, []).append(done[j] - done[j - 1])
+    print("own-bound chunk period by rows (64-row bins): " + ", ".join(
+        f"{64 * k}-{64 * k + 63}: p50 {np.median(v):.0f} ns (n={len(v)})" for k, v in sorted(per_rows.items())))
+    # parts of the own-bound period: prefetch done (words 56..), barrier passed (9+3w), done
+    gmax = min(info.get("group") or 1, 8)
+    pre = np.where(T[:, 56:56 + gmax] >= 0, T[:, 56:56 + gmax], -1).max(axis=1)
+    bar = T[:, 9:9 + 3 * nw:3].max(axis=1)
+    parts = {"prefetch_done - prev_done": [], "barrier - prev_done": [], "done - barrier": [],
+             "ready - prev_done": [], "landed - prev_done": []}
+    for c in range(ncta):
+        for j in range(c0[c] + 1, c0[c + 1]):
+            if ready[j] <= done[j - 1]:
+                parts["prefetch_done - prev_done"].append(pre[j] - done[j - 1])
+                parts["barrier - prev_done"].append(bar[j] - done[j - 1])
+                parts["done - barrier"].append(done[j] - bar[j])
+                parts["ready - prev_done"].append(ready[j] - done[j - 1])
+                parts["landed - prev_done"].append(landed[j] - done[j - 1])
+    for k, v in parts.items():
+        print(f"  own-bound {k}: p10 {np.percentile(v, 10):.0f} p50 {np.median(v):.0f} p90 {np.percentile(v, 90):.0f} ns")
+    st = tr[:, 48:54].astype(np.int64)
+    # warp 0 (group 0) stamps its chunks only: local chunk index divisible by the group count
+    K = max(info.get("groups") or 1, 1)
+    local = np.concatenate([np.arange(c0[c + 1] - c0[c]) for c in range(ncta)])
+    sel = (local % K == 0) & (st[:, 1] > 0)
+    if sel.any():
+        print("  warp-0 SM-clock stamps after its barrier (cycles, p50): " + ", ".join(
+            f"{n} {np.median(st[sel, k]):.0f}" for k, n in ((1, "gathers"), (2, "fp"), (3, "stores"),
+                                                            (4, "bar.arrive"), (5, "x stores"))))
     bins = np.linspace(0, total, 11)
     act = [int(np.sum((first <= b1) & (last >= b0))) for b0, b1 in zip(bins[:-1], bins[1:])]
     print("active CTAs per tenth of the solve:", act)
