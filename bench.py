@@ -213,8 +213,9 @@ def measure_config(H, torch, name, args, world, device, with_cpu):
     u_ms = [e[1].elapsed_time(e[2]) for e in ev]
     apply_same = bool((xp.cpu().numpy().view(np.uint64) == x.cpu().numpy().view(np.uint64)).all())
     # the dominant kernel alone: k_wave (L) from an already permuted right-hand side
-    bp = torch.empty(pl.n + 2, dtype=torch.float64, device=device)
-    yw = torch.empty_like(y)
+    wl = info_l["wave_len"]
+    bp = torch.empty(wl + 2, dtype=torch.float64, device=device)
+    yw = torch.empty(wl, dtype=torch.float64, device=device)
     tl.permute_in(b, bp, stream)
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
@@ -266,7 +267,7 @@ def measure_config(H, torch, name, args, world, device, with_cpu):
             "workload": cfg["workload"], "n": pl.n, "nnz_L": int(f.l.nnz()), "nnz_U": int(f.u.nnz()),
             "nlev_L": int(pl.schedule.nlev), "nlev_U": int(pu.schedule.nlev), "ell_width": int(pl.hec.ell.width),
             "alg_bytes_per_step": alg, "strategy": "pipeline" if info_l["strategy"] == 2 else "levels",
-            "layout_L": {0: "slabs", 1: "z-pencils", 2: "strips"}.get(info_l["layout"], "levels"),
+            "layout_L": {0: "slabs", 1: "z-pencils", 2: "strips", 4: "columns"}.get(info_l["layout"], "levels"),
             "solver_shape_L": f"{info_l['group']}x{info_l['groups']}x{info_l['rows_per_lane']}",
             "ctas": info_l["ctas"], "chunks_L": info_l["chunks"], "chunks_U": info_u["chunks"],
             "l2": "inputs larger than L2 (%.0f MB of factors per step vs 126 MB L2)" % (alg / 1e6),

@@ -74,10 +74,15 @@ typedef struct {
     double predicted_us; /* cost-model critical path of one solve               */
     /* PIPELINE layout actually built (diagnostics; -1 / 0 for LEVELS) */
     int layout;          /* 0 slabs, 1 z-pencils (recognised grid), 2 strips,     */
-                         /* 3 mirror of the L layout (U of an ILU pair)           */
+                         /* 3 mirror of the L layout (U of an ILU pair),          */
+                         /* 4 columns (7-point grid: one lane per grid column),   */
+                         /* 5 columns, mirror of the L layout                     */
     int group, groups, rows_per_lane; /* solver shape G x K x RPL               */
     int width;           /* sliced-ELL width W of the device blob                */
     int ring, halo_ring, inflight;    /* shared-memory rings, descriptor slots  */
+    long long wave_len;  /* entries of the wave-ordered vectors: bp holds        */
+                         /* wave_len + 2, xw wave_len (n, except the column      */
+                         /* layout, whose slots include padding)                 */
 } hec_tri_info;
 
 typedef struct hec_tri* hec_tri_t;
@@ -99,7 +104,12 @@ int hec_tri_create(int n, int reversal_applied, int nlev, const int* level_start
  * x = T^-1 b in the original ordering, device pointers, enqueued on `stream`
  * (cudaStream_t; NULL = legacy default stream). Bitwise equal to the
  * reference's hec::solve (proj/src/triangular.cpp:90-135) for any worker count.
- * b and x must not alias. Concurrent solves on different streams are allowed.
+ * b and x must not alias. Concurrent solves on different streams are allowed:
+ * each stream gets its own workspace (tickets, epoch, mailboxes). A CUDA graph
+ * captured on a stream keeps that stream's workspace, so a replay must not
+ * overlap another solve enqueued on the capture stream, nor a replay of another
+ * graph captured on the same stream (serialise them, or capture on distinct
+ * streams).
  */
 int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream);
 
@@ -108,8 +118,8 @@ int hec_tri_solve(hec_tri_t t, const double* b_dev, double* x_dev, void* stream)
  * right-hand side in the layout's private row order (the reference's
  * permute-in, proj/src/triangular.cpp:110-111, into the order the persistent
  * kernel consumes: CTA, chunk, row), then the solve from bp. That order is
- * OPAQUE: only hec_tri_permute_in produces a valid bp. bp must hold n + 2
- * doubles and be 16-byte aligned (the kernel moves it with bulk copies);
+ * OPAQUE: only hec_tri_permute_in produces a valid bp. bp must hold
+ * info.wave_len + 2 doubles (hec_tri_query) and be 16-byte aligned (the kernel moves it with bulk copies);
  * otherwise HEC_EINVAL.
  */
 int hec_tri_permute_in(hec_tri_t t, const double* b_dev, double* bp_dev, void* stream);
@@ -119,7 +129,7 @@ int hec_tri_solve_ordered(hec_tri_t t, const double* bp_dev, double* x_dev, void
  * hec_tri_permute_out gathers x[o] = xw[wpos[o]] (the reference's permute-out,
  * proj/src/triangular.cpp:131-132). A consumer that can read the wave order
  * directly (the U solve of an ILU apply) skips the second pass. */
-int hec_tri_solve_wave(hec_tri_t t, const double* bp_dev, double* xw_dev, void* stream); /* bp: as above */
+int hec_tri_solve_wave(hec_tri_t t, const double* bp_dev, double* xw_dev, void* stream); /* bp: as above; xw: wave_len */
 int hec_tri_permute_out(hec_tri_t t, const double* xw_dev, double* x_dev, void* stream);
 
 /* Same with host vectors (H2D, solve, D2H; synchronous). Drop-in for hec::solve. */

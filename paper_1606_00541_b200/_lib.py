@@ -36,7 +36,7 @@ class TriInfo(C.Structure):
                 ("threads", c_int), ("chunks", c_int), ("nnz", c_ll), ("device_bytes", c_ll),
                 ("alg_bytes", c_dbl), ("predicted_us", c_dbl), ("layout", c_int), ("group", c_int),
                 ("groups", c_int), ("rows_per_lane", c_int), ("width", c_int), ("ring", c_int),
-                ("halo_ring", c_int), ("inflight", c_int)]
+                ("halo_ring", c_int), ("inflight", c_int), ("wave_len", c_ll)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

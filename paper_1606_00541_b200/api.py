@@ -417,7 +417,7 @@ class DeviceTri:
                                 C.c_void_p(_stream(stream)) if stream is not None else None))
 
     def permute_in(self, b_dev, bp_dev, stream=None) -> None:
-        """bp[r] = b[input index of reordered row r]; bp holds n + 2 doubles."""
+        """bp in the layout's private order; bp holds info()["wave_len"] + 2 doubles."""
         check(lib.hec_tri_permute_in(self._h, C.c_void_p(_ptr(b_dev)), C.c_void_p(_ptr(bp_dev)),
                                      C.c_void_p(_stream(stream)) if stream is not None else None))
 

@@ -312,6 +312,7 @@ void fill_info(const hec::dev::TriStats& s, hec_tri_info* info) {
     info->ring = s.ring;
     info->halo_ring = s.halo_ring;
     info->inflight = s.slots;
+    info->wave_len = s.wave_len;
 }
 
 hec::WidthPolicy policy_of(int mode, int width) {

@@ -48,7 +48,8 @@ inline int rup(int v, int m) { return (v + m - 1) / m * m; }
 }  // namespace
 
 // ------------------------------------------------------------ DeviceTri ----
-DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror) {
+DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror,
+                     const plan::ColMirror* cmirror) {
     require_device();
     plan::validate(src);
     n_ = src.n;
@@ -103,9 +104,29 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
         const int budget = smem_optin() - 1024;  // static shared + slack
         cfg.smem_bytes = budget;
         cfg.ctrl_bytes = kWaveCtrlBytes;
+        // 7-point grid factors: the column-state kernel (HEC_WAVE_COLUMNS=1; experimental, off by default)
+        const char* ce = std::getenv("HEC_WAVE_COLUMNS");
+        if (ce && std::atoi(ce) != 0 && cfg.pencils && !mirror && !std::getenv("HEC_WAVE_G")) {
+            plan::ColConfig cc;
+            cc.ctas = cfg.ctas;
+            cc.smem_bytes = budget;
+            if (const char* e = std::getenv("HEC_COLS_WARPS")) cc.warps = std::atoi(e);
+            if (const char* e = std::getenv("HEC_COLS_RING")) cc.ring_max = std::min(16, std::max(3, std::atoi(e)));
+            auto try_cols = [&](const plan::ColMirror* cm) {
+                cc.mirror = cm;
+                try {
+                    build_columns(plan::build_columns(src, cc));
+                } catch (const std::invalid_argument& e) {
+                    if (std::getenv("HEC_DEBUG"))
+                        std::fprintf(stderr, "[hec] no column layout%s: %s\n", cm ? " (mirror)" : "", e.what());
+                }
+            };
+            if (cmirror) try_cols(cmirror);  // U of an ILU pair: L's slots reversed
+            if (!cols_) try_cols(nullptr);
+        }
         plan::WaveLayout P;
-        bool ok = true;
-        try {
+        bool ok = !cols_;
+        if (ok) try {
             if (mirror) {
                 cfg.mirror = mirror;
                 try {
@@ -118,6 +139,10 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
             if (!cfg.mirror) P = plan::build_wave(src, cfg);
         } catch (const std::invalid_argument&) {
             ok = false;  // row order the wave layout cannot schedule: level launches
+        }
+        if (cols_) {
+            stats_.strategy = strategy_;
+            return;
         }
         p_ring_ = ok ? P.ring : cfg.ring;
         p_ring_off_ = kWaveCtrlBytes;
@@ -151,6 +176,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
             p_cta0_host_ = P.cta_chunk0;
             h_chunk_r0_ = P.chunk_r0;
             mirrored_ = P.mirrored;
+            wave_len_ = n_;
             p_wpos_.upload(P.wpos);
             h_wpos_ = P.wpos;
             h_bidx_ = P.bidx;
@@ -194,9 +220,104 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
                  L.tail_dep.size()) +
             8 * (L.ell_val.size() + L.diag.size() + L.tail_val.size()));
         stats_.threads = 256;
+        wave_len_ = n_;
         spare_ = make_workspace();
     }
+    stats_.wave_len = wave_len_;
     stats_.strategy = strategy_;
+}
+
+void DeviceTri::build_columns(const plan::ColLayout& C) {
+    void* k = cols_kernel(C.warps, C.unit, false, C.order);
+    void* kt = cols_kernel(C.warps, C.unit, true, C.order);
+    if (!k || !kt) throw std::invalid_argument("columns: no kernel for this warp count");
+    const int smem = plan::kColCtrlBytes + C.ring * (C.block_bytes + 8 * C.lanes);
+    HEC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    HEC_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cols_ = true;
+    c_info_ = C.mirror_info();
+    c_blocks_.upload(C.blocks);
+    c_cta_.upload(C.cta);
+    c_block_bytes_ = C.block_bytes;
+    c_ring_ = C.ring;
+    c_warps_ = C.warps;
+    c_unit_ = C.unit;
+    p_kernel_ = k;
+    p_kernel_trace_ = kt;
+    p_smem_ = smem;
+    p_ctas_ = C.ctas;
+    p_warps_ = C.warps;
+    p_exports_ = C.mailboxes;
+    mirrored_ = C.mirrored;
+    wave_len_ = C.slots;
+    // the permute pass writes bp in the order the kernel reads it: a mirrored
+    // layout reads slot s from bp[S-1-s]
+    h_bidx_ = C.bidx;
+    if (mirrored_) std::reverse(h_bidx_.begin(), h_bidx_.end());
+    p_bidx_.upload(h_bidx_);
+    h_wpos_ = C.wpos;
+    p_wpos_.upload(h_wpos_);
+    p_cta0_host_.resize(C.ctas + 1);  // level-block range of each CTA (diagnostics)
+    for (int c = 0; c < C.ctas; ++c) p_cta0_host_[c] = C.cta[4 * c + 3];
+    p_cta0_host_[C.ctas] = static_cast<int>(C.total_levels);
+    stats_.ctas = C.ctas;
+    stats_.threads = 32 * C.warps;
+    stats_.chunks = static_cast<int>(C.total_levels);
+    stats_.slots = C.ring;
+    stats_.layout = C.mirrored ? 5 : 4;
+    stats_.group = C.warps;
+    stats_.groups = 1;
+    stats_.rpl = 1;
+    stats_.width = 3;
+    stats_.ring = C.ring;
+    stats_.halo_ring = 0;
+    stats_.wave_len = C.slots;
+    stats_.device_bytes = static_cast<long long>(C.blocks.size() + 4 * C.cta.size() + 4 * C.bidx.size() +
+                                                 4 * C.wpos.size() + 16 * C.mailboxes);
+    if (std::getenv("HEC_DEBUG"))
+        std::fprintf(stderr, "[hec] columns n=%d grid=%dx%dx%d tiles=%dx%d warps=%dx%d ctas=%d slots=%lld levels=%lld "
+                     "ring=%d block=%d unit=%d mirrored=%d order=%d,%d,%d\n", C.n, C.nx, C.ny, C.nz, C.PX, C.PY, C.WX,
+                     C.WY, C.ctas, C.slots, C.total_levels, C.ring, C.block_bytes, C.unit ? 1 : 0, C.mirrored ? 1 : 0,
+                     C.order & 3, (C.order >> 2) & 3, (C.order >> 4) & 3);
+    spare_ = make_workspace();
+}
+
+bool DeviceTri::col_mirror_info(plan::ColMirror& m) const {
+    if (!cols_) return false;
+    m = c_info_;
+    return true;
+}
+
+void DeviceTri::launch_cols(const double* bp, double* xw, cudaStream_t st, unsigned long long* trace) {
+    Workspace& w = workspace(st);
+    ColArgs a{};
+    a.blocks = c_blocks_.p;
+    a.cta = reinterpret_cast<const int4*>(c_cta_.p);
+    a.bp = bp;
+    a.xw = xw;
+    a.mbox = w.mailbox.p;
+    a.counters = w.counters.p;
+    a.slots = wave_len_;
+    a.ctas = p_ctas_;
+    a.nx = c_info_.nx;
+    a.ny = c_info_.ny;
+    a.nz = c_info_.nz;
+    a.WX = c_info_.WX;
+    a.WY = c_info_.WY;
+    a.PX = c_info_.PX;
+    a.PY = c_info_.PY;
+    a.ox = c_info_.ox;
+    a.oy = c_info_.oy;
+    a.mbox_top0 = static_cast<long long>(p_ctas_) * (4 * a.WY) * a.nz;
+    a.block_bytes = c_block_bytes_;
+    a.ring = c_ring_;
+    a.bp_reversed = mirrored_ ? 1 : 0;
+    a.watchdog_cycles = watchdog_ns_ / 1000000ULL * static_cast<unsigned long long>(clock_khz_);
+    a.order = c_info_.order;
+    a.trace = trace;
+    void* args[] = {&a};
+    HEC_CUDA(cudaLaunchCooperativeKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_), dim3(32 * c_warps_),
+                                         args, p_smem_, st));
 }
 
 DeviceTri::~DeviceTri() {
@@ -233,8 +354,8 @@ std::unique_ptr<DeviceTri::Workspace> DeviceTri::make_workspace() const {
     const uint32_t init[3] = {0u, 0u, 1u};
     HEC_CUDA(cudaMemcpy(w->counters.p, init, sizeof(init), cudaMemcpyHostToDevice));
     w->mailbox.alloc(2 * static_cast<std::size_t>(std::max<long long>(p_exports_, 1)));
-    w->bp.alloc(static_cast<std::size_t>(std::max(n_, 1)) + 2);
-    w->xw.alloc(static_cast<std::size_t>(std::max(n_, 1)));
+    w->bp.alloc(static_cast<std::size_t>(std::max<long long>(wave_len_, 1)) + 2);
+    w->xw.alloc(static_cast<std::size_t>(std::max<long long>(wave_len_, 1)));
     HEC_CUDA(cudaMemset(w->mailbox.p, 0, sizeof(unsigned long long) * w->mailbox.count));  // epoch 0: empty
     HEC_CUDA(cudaDeviceSynchronize());
     return w;
@@ -268,7 +389,7 @@ void DeviceTri::release_workspace(cudaStream_t st) {
 
 void DeviceTri::permute(const double* b, double* bp, cudaStream_t st) const {
     if (n_ == 0) return;
-    permute_in(b, strategy_ == 1 ? l_bidx_.p : p_bidx_.p, bp, n_, st);
+    permute_in(b, strategy_ == 1 ? l_bidx_.p : p_bidx_.p, bp, strategy_ == 1 ? n_ : static_cast<int>(wave_len_), st);
     HEC_CUDA(cudaGetLastError());
 }
 
@@ -344,6 +465,10 @@ void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream
     if (n_ == 0) return;
     if (strategy_ == 1) {
         run_levels(bp, true, xw, out, st);
+        return;
+    }
+    if (cols_) {
+        launch_cols(bp, xw, st, trace);
         return;
     }
     Workspace& w = workspace(st);
@@ -443,8 +568,12 @@ DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* ow
 // the solves); otherwise its own layout plus the composed gather.
 void DevicePrecond::build_upper(const plan::TriSource& u, const TriOptions& opt) {
     plan::WaveMirror m;
-    const bool can = l_->mirror_info(m) && !std::getenv("HEC_NO_MIRROR");
-    u_ = std::make_unique<DeviceTri>(u, opt, can ? &m : nullptr);
+    plan::ColMirror cm;
+    const bool no = std::getenv("HEC_NO_MIRROR") != nullptr;
+    if (!no && l_->col_mirror_info(cm))
+        u_ = std::make_unique<DeviceTri>(u, opt, nullptr, &cm);
+    else
+        u_ = std::make_unique<DeviceTri>(u, opt, (!no && l_->mirror_info(m)) ? &m : nullptr);
     if (!u_->mirrored()) compose();
 }
 
@@ -457,10 +586,12 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
     auto& w = ws_[st];
     if (!w) {
         w = std::make_unique<Workspace>();
-        w->bl.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
-        w->yw.alloc(std::max(n_ext_, 1));
-        w->bu.alloc(static_cast<std::size_t>(std::max(n_ext_, 1)) + 2);
-        w->xw.alloc(std::max(n_ext_, 1));
+        const std::size_t ll = static_cast<std::size_t>(std::max<long long>(l_->wave_len(), 1));
+        const std::size_t lu = static_cast<std::size_t>(std::max<long long>(u_->wave_len(), 1));
+        w->bl.alloc(ll + 2);
+        w->yw.alloc(ll);
+        w->bu.alloc(lu + 2);
+        w->xw.alloc(lu);
     }
     return *w;
 }
@@ -475,7 +606,7 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
     l_->solve_wave(w.bl.p, w.yw.p, nullptr, st);
     const double* bu = w.yw.p;  // mirrored U: L's output as it lies
     if (!u_->mirrored()) {
-        permute_in(w.yw.p, lu_map_.p, w.bu.p, n_ext_, st);
+        permute_in(w.yw.p, lu_map_.p, w.bu.p, static_cast<int>(u_->wave_len()), st);
         HEC_CUDA(cudaGetLastError());
         bu = w.bu.p;
     }
@@ -489,8 +620,8 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
 void DevicePrecond::compose() {
     const std::vector<int>& bu = u_->host_bidx();
     const std::vector<int>& wl = l_->host_wpos();
-    std::vector<int> m(static_cast<std::size_t>(n_ext_));
-    for (int p = 0; p < n_ext_; ++p) m[p] = wl.empty() ? bu[p] : wl[bu[p]];
+    std::vector<int> m(bu.size());
+    for (std::size_t p = 0; p < bu.size(); ++p) m[p] = wl.empty() ? bu[p] : wl[bu[p]];
     lu_map_.upload(m);
 }
 

@@ -67,7 +67,7 @@ struct TriOptions {
 struct TriStats {
     int n = 0, nlev = 0, strategy = 0, ctas = 0, threads = 0, chunks = 0, slots = 0;
     int layout = -1, group = 0, groups = 0, rpl = 0, width = 0, ring = 0, halo_ring = 0;
-    long long nnz = 0, device_bytes = 0;
+    long long nnz = 0, device_bytes = 0, wave_len = 0;
     double alg_bytes = 0.0, predicted_us = 0.0;
 };
 
@@ -75,7 +75,9 @@ class DeviceTri {
 public:
     // mirror: build the wave layout as the exact mirror of another one (the L of
     // an ILU pair) when valid (plan::WaveMirror), else the layout of its own
-    DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror = nullptr);
+    // cmirror: likewise for the column layout (tri_plan.hpp COLUMNS)
+    DeviceTri(const plan::TriSource& src, const TriOptions& opt, const plan::WaveMirror* mirror = nullptr,
+              const plan::ColMirror* cmirror = nullptr);
     ~DeviceTri();
     DeviceTri(const DeviceTri&) = delete;
     DeviceTri& operator=(const DeviceTri&) = delete;
@@ -99,7 +101,11 @@ public:
     const std::vector<int>& host_wpos() const { return h_wpos_; }
     // this layout's chunk structure, for mirroring (false for level launches)
     bool mirror_info(plan::WaveMirror& m) const;
+    // the column layout's tiling, for mirroring (false for any other layout)
+    bool col_mirror_info(plan::ColMirror& m) const;
     bool mirrored() const { return mirrored_; }
+    // entries of the wave-ordered vectors (bp holds wave_len() + 2, xw wave_len())
+    long long wave_len() const { return wave_len_; }
     // chunk -> CTA map of the pipeline layout (empty for LEVELS)
     const std::vector<int>& cta_chunk0() const { return p_cta0_host_; }
     // Synchronous host-vector convenience (pinned or pageable).
@@ -149,6 +155,16 @@ private:
     long long p_exports_ = 0;
     std::vector<int> p_cta0_host_, h_chunk_r0_;
     bool mirrored_ = false;
+    long long wave_len_ = 0;
+    // COLUMNS (k_cols, 7-point grids)
+    bool cols_ = false;
+    plan::ColMirror c_info_;
+    DevBuf<unsigned char> c_blocks_;
+    DevBuf<int> c_cta_;
+    int c_block_bytes_ = 0, c_ring_ = 0, c_warps_ = 0;
+    bool c_unit_ = false;
+    void build_columns(const plan::ColLayout& C);
+    void launch_cols(const double* bp, double* xw, cudaStream_t st, unsigned long long* trace);
 
     std::mutex mu_;
     std::map<cudaStream_t, std::unique_ptr<Workspace>> ws_;

@@ -50,6 +50,25 @@ struct WaveArgs {
     unsigned long long* trace;   // diagnostics: 16 words per chunk (TRACE kernel only)
 };
 
+// k_cols (cols_kernel.cu; layout: tri_plan.hpp COLUMNS)
+struct ColArgs {
+    const unsigned char* blocks;  // one block per (CTA, level): val[3][lanes], (diag, rcp)[lanes], code[lanes]
+    const int4* cta;              // per CTA: first level, level count, first slot / lanes, first block
+    const double* bp;             // right-hand side in slot order (bp_reversed: slot s reads bp[slots-1-s])
+    double* xw;                   // solution in slot order
+    unsigned long long* mbox;     // tile-edge mailboxes, 2 epoch-tagged words each
+    uint32_t* counters;           // as WaveArgs::counters
+    long long slots;
+    long long mbox_top0;          // first top-edge mailbox (right-edge ones come first)
+    int ctas, nx, ny, nz, WX, WY, PX, PY, ox, oy;
+    int block_bytes, ring, bp_reversed;
+    int order;                    // entry order shared by all rows (plan::ColLayout::order)
+    unsigned long long watchdog_cycles;
+    unsigned long long* trace;    // diagnostics (trace kernel): 4 words per CTA level (warp 0, lane 0)
+};
+void* cols_kernel(int warps, bool unit, bool trace, int order);
+constexpr int kColOrderZYX = 2 | 1 << 2 | 0 << 4;  // (z-1, y-1, x-1): natural-order 7-point factors
+
 // one launch per level, arguments read from dev_args (capturable once, replayed for any vectors)
 void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, int nlev, cudaStream_t st);
 void set_level_args(const LevelArgs& a, LevelArgs* dev, cudaStream_t st);

@@ -902,4 +902,185 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
     return P;
 }
 
+// ---------------------------------------------------------------- COLUMNS ----
+ColLayout build_columns(const TriSource& s, const ColConfig& cfg) {
+    validate(s);
+    if (s.b_map || s.out_map) throw std::invalid_argument("columns: RAS maps");
+    const GridGeom g = detect_grid(s);
+    const int n = s.n;
+    if (!g.ok || static_cast<long long>(g.nx) * g.ny * g.nz != n) throw std::invalid_argument("columns: no grid");
+    const int nx = g.nx, ny = g.ny, nz = g.nz, plane = nx * ny;
+    // every row: entries among (x-1), (y-1), (z-1) only, in any order; codes per entry
+    std::vector<int> r_of(n);
+    for (int r = 0; r < n; ++r) r_of[s.inv_perm[r]] = r;
+    // rank[i][dir]: position of the entry towards neighbour dir in row i's solve
+    // order (-1: absent). The kernel subtracts the present entries in one order
+    // shared by all rows, so every row must agree with it.
+    std::vector<unsigned char> code(n, 0);  // presence mask: 1 left (x-1), 2 down (y-1), 4 back (z-1)
+    std::vector<signed char> seq(3 * static_cast<std::size_t>(n), -1);
+    int bad = 0, nonunit = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad, nonunit)
+    for (int i = 0; i < n; ++i) {
+        const int r = r_of[i];
+        const int x = i % nx, y = (i / nx) % ny, z = i / plane;
+        int u = 0;
+        unsigned m = 0;
+        bool ok = true;
+        for_each_entry(s, r, [&](int col, double) {
+            const int d = i - s.inv_perm[col];
+            int dir = -1;
+            if (d == 1 && x > 0) dir = 0;
+            else if (d == nx && y > 0) dir = 1;
+            else if (d == plane && z > 0) dir = 2;
+            if (dir < 0 || u >= 3 || (m >> dir) & 1u) {
+                ok = false;
+                return;
+            }
+            m |= 1u << dir;
+            seq[3 * static_cast<std::size_t>(i) + u] = static_cast<signed char>(dir);
+            ++u;
+        });
+        if (!ok) ++bad;
+        code[i] = static_cast<unsigned char>(m);
+        const double dg = s.csr_vals[s.csr_rp[r + 1] - 1];
+        if (!(dg == 1.0 && !std::signbit(dg))) ++nonunit;
+    }
+    if (bad) throw std::invalid_argument("columns: not a 7-point grid factor");
+    int order[3] = {-1, -1, -1};  // the common entry order (directions), from a row with all three
+    for (int i = 0; i < n && order[0] < 0; ++i)
+        if (code[i] == 7)
+            for (int u = 0; u < 3; ++u) order[u] = seq[3 * static_cast<std::size_t>(i) + u];
+    if (order[0] < 0) throw std::invalid_argument("columns: no interior row");
+    int pos[3];
+    for (int u = 0; u < 3; ++u) pos[order[u]] = u;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
+    for (int i = 0; i < n; ++i) {  // present entries in increasing common position
+        int prev = -1;
+        for (int u = 0; u < 3; ++u) {
+            const int d = seq[3 * static_cast<std::size_t>(i) + u];
+            if (d < 0) break;
+            if (pos[d] <= prev) ++bad;
+            prev = pos[d];
+        }
+    }
+    if (bad) throw std::invalid_argument("columns: rows disagree on the entry order");
+    ColLayout P;
+    P.n = n;
+    P.nx = nx;
+    P.ny = ny;
+    P.nz = nz;
+    P.nlev = nx + ny + nz - 2;
+    P.unit = nonunit == 0;
+    P.order = order[0] | order[1] << 2 | order[2] << 4;
+    constexpr int SX = ColLayout::SX, SY = ColLayout::SY;
+    if (cfg.mirror) {
+        const ColMirror& m = *cfg.mirror;
+        if (m.nx != nx || m.ny != ny || m.nz != nz || !s.reversed) throw std::invalid_argument("columns: no mirror");
+        P.WX = m.WX;
+        P.WY = m.WY;
+        P.PX = m.PX;
+        P.PY = m.PY;
+        P.ox = m.PX * SX * m.WX - nx - m.ox;
+        P.oy = m.PY * SY * m.WY - ny - m.oy;
+        P.mirrored = true;
+    } else {
+        // tiling: one CTA per SM at most; the level chain costs ~max(300, 0.6 * lanes)
+        // cycles a level, each CTA boundary a wavefront crosses ~2000 cycles of lag
+        double best = 1e300;
+        for (int nw : {16, 8, 4, 2, 1}) {
+            if (cfg.warps > 0 && nw != cfg.warps) continue;
+            for (int wx = 1; wx <= nw; wx *= 2) {
+                const int wy = nw / wx;
+                const int tx = SX * wx, ty = SY * wy;
+                const int px = (nx + tx - 1) / tx, py = (ny + ty - 1) / ty;
+                if (static_cast<long long>(px) * py > cfg.ctas) continue;
+                const double est = P.nlev * std::max(300.0, 0.6 * 32 * nw) + 2000.0 * (px + py - 2);
+                if (est < best) {
+                    best = est;
+                    P.WX = wx;
+                    P.WY = wy;
+                    P.PX = px;
+                    P.PY = py;
+                }
+            }
+        }
+        if (best >= 1e300) throw std::invalid_argument("columns: no tiling fits the CTA count");
+    }
+    const int TX = SX * P.WX, TY = SY * P.WY, C = P.PX * P.PY;
+    P.ctas = C;
+    P.warps = P.WX * P.WY;
+    P.lanes = 32 * P.warps;
+    const int NS = P.lanes;
+    P.block_bytes = round_up((P.unit ? 24 : 40) * NS + NS, 16);
+    const int per_level = P.block_bytes + 8 * NS;
+    P.ring = cfg.smem_bytes > 0 ? std::min(cfg.ring_max, (cfg.smem_bytes - kColCtrlBytes) / per_level) : 8;
+    if (P.ring < 3) throw std::invalid_argument("columns: level blocks exceed shared memory");
+    P.cta.assign(4 * static_cast<std::size_t>(C), 0);
+    long long slot = 0, blk = 0;
+    for (int c = 0; c < C; ++c) {
+        const int px = c % P.PX, py = c / P.PX;
+        const int xs = std::max(0, px * TX - P.ox), xe = std::min(nx, (px + 1) * TX - P.ox);
+        const int ys = std::max(0, py * TY - P.oy), ye = std::min(ny, (py + 1) * TY - P.oy);
+        if (xs >= xe || ys >= ye) throw std::invalid_argument("columns: empty tile");
+        const int l0 = xs + ys, nl = (xe - 1) + (ye - 1) + (nz - 1) - l0 + 1;
+        if (slot / NS > INT32_MAX || blk > INT32_MAX) throw std::overflow_error("columns: layout too large");
+        P.cta[4 * c] = l0;
+        P.cta[4 * c + 1] = nl;
+        P.cta[4 * c + 2] = static_cast<int>(slot / NS);
+        P.cta[4 * c + 3] = static_cast<int>(blk);
+        slot += static_cast<long long>(nl) * NS;
+        blk += nl;
+    }
+    if (slot > INT32_MAX - 64) throw std::overflow_error("columns: more than 2^31 slots");
+    if (cfg.mirror && slot != cfg.mirror->slots) throw std::invalid_argument("columns: mirror slot count");
+    P.slots = slot;
+    P.total_levels = blk;
+    P.mailboxes = static_cast<long long>(C) * (TX + TY) * nz;
+    P.blocks.assign(static_cast<std::size_t>(blk) * P.block_bytes, 0);
+    P.bidx.assign(static_cast<std::size_t>(slot), 0);
+    P.wpos.assign(n, 0);
+    const int off_code = (P.unit ? 24 : 40) * NS;
+#pragma omp parallel for schedule(static)
+    for (long long b = 0; b < blk; ++b) {  // padding: no entries, diagonal 1
+        unsigned char* q = P.blocks.data() + static_cast<std::size_t>(b) * P.block_bytes;
+        if (!P.unit)
+            for (int k = 0; k < NS; ++k) {
+                const double one = 1.0;
+                std::memcpy(q + 24 * NS + 8 * k, &one, 8);
+                std::memcpy(q + 32 * NS + 8 * k, &one, 8);
+            }
+    }
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+        const int r = r_of[i];
+        const int x = i % nx, y = (i / nx) % ny, z = i / plane;
+        const int ax = x + P.ox, ay = y + P.oy;
+        const int px = ax / TX, py = ay / TY, c = py * P.PX + px;
+        const int wx = (ax % TX) / SX, lx = ax % SX, wy = (ay % TY) / SY, ly = ay % SY;
+        const int k = (wy * P.WX + wx) * 32 + ly * SX + lx;
+        const int l = x + y + z - P.cta[4 * c];
+        const long long sl = static_cast<long long>(P.cta[4 * c + 2]) * NS + static_cast<long long>(l) * NS + k;
+        unsigned char* q = P.blocks.data() + (static_cast<std::size_t>(P.cta[4 * c + 3]) + l) * P.block_bytes;
+        int u = 0;
+        unsigned m = 0;
+        for_each_entry(s, r, [&](int, double v) {  // entry towards neighbour dir -> its common position
+            const int p = pos[seq[3 * static_cast<std::size_t>(i) + u]];
+            std::memcpy(q + 8 * (static_cast<std::size_t>(p) * NS + k), &v, 8);
+            m |= 1u << p;
+            ++u;
+        });
+        q[off_code + k] = static_cast<unsigned char>(m);
+        if (!P.unit) {
+            const double d = s.csr_vals[s.csr_rp[r + 1] - 1];
+            const double rc = 1.0 / d;  // RN(1/d), as __drcp_rn
+            std::memcpy(q + 24 * NS + 8 * k, &d, 8);
+            std::memcpy(q + 32 * NS + 8 * k, &rc, 8);
+        }
+        const int o = s.reversed ? n - 1 - i : i;
+        P.bidx[static_cast<std::size_t>(sl)] = o;
+        P.wpos[o] = static_cast<int>(sl);
+    }
+    return P;
+}
+
 }  // namespace hec::plan

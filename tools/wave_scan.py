@@ -29,8 +29,6 @@ def main():
         f = H.ilu0(a)
         p = H.prepare_lower(f.l) if args.which == "L" else H.prepare_upper(f.u)
         nnz = p.hec.ell.width * p.n
-        bp = torch.ones(p.n + 2, dtype=torch.float64, device="cuda")
-        xw = torch.empty(p.n, dtype=torch.float64, device="cuda")
         for shape in (args.shapes.split(",") if args.shapes else [""]):
             if shape:
                 G, K, R = shape.split("x")
@@ -42,6 +40,8 @@ def main():
                     print(f"{st}-pt {s}^3 {args.which} shape {shape or 'auto'} ctas {c}: {e}")
                     continue
                 info = t.info()
+                bp = torch.ones(info["wave_len"] + 2, dtype=torch.float64, device="cuda")
+                xw = torch.empty(info["wave_len"], dtype=torch.float64, device="cuda")
                 for _ in range(3):
                     t.solve_wave(bp, xw)
                 torch.cuda.synchronize()
