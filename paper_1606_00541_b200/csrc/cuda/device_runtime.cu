@@ -111,7 +111,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
             cc.ctas = cfg.ctas;
             cc.smem_bytes = budget;
             if (const char* e = std::getenv("HEC_COLS_WARPS")) cc.warps = std::atoi(e);
-            if (const char* e = std::getenv("HEC_COLS_RING")) cc.ring_max = std::min(16, std::max(3, std::atoi(e)));
+            if (const char* e = std::getenv("HEC_COLS_RPL")) cc.rpl = std::atoi(e);
+            if (const char* e = std::getenv("HEC_COLS_RING")) cc.ring_max = std::min(plan::kColEdgeLevels - 2, std::max(3, std::atoi(e)));
             auto try_cols = [&](const plan::ColMirror* cm) {
                 cc.mirror = cm;
                 try {
@@ -228,8 +229,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
 }
 
 void DeviceTri::build_columns(const plan::ColLayout& C) {
-    void* k = cols_kernel(C.warps, C.unit, false, C.order);
-    void* kt = cols_kernel(C.warps, C.unit, true, C.order);
+    void* k = cols_kernel(C.warps, C.rpl, C.unit, false, C.order);
+    void* kt = cols_kernel(C.warps, C.rpl, C.unit, true, C.order);
     if (!k || !kt) throw std::invalid_argument("columns: no kernel for this warp count");
     const int smem = plan::kColCtrlBytes + C.ring * (C.block_bytes + 8 * C.lanes);
     HEC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -261,13 +262,13 @@ void DeviceTri::build_columns(const plan::ColLayout& C) {
     for (int c = 0; c < C.ctas; ++c) p_cta0_host_[c] = C.cta[4 * c + 3];
     p_cta0_host_[C.ctas] = static_cast<int>(C.total_levels);
     stats_.ctas = C.ctas;
-    stats_.threads = 32 * C.warps;
+    stats_.threads = 32 * (C.warps + 1);
     stats_.chunks = static_cast<int>(C.total_levels);
     stats_.slots = C.ring;
     stats_.layout = C.mirrored ? 5 : 4;
     stats_.group = C.warps;
     stats_.groups = 1;
-    stats_.rpl = 1;
+    stats_.rpl = C.rpl;
     stats_.width = 3;
     stats_.ring = C.ring;
     stats_.halo_ring = 0;
@@ -275,9 +276,9 @@ void DeviceTri::build_columns(const plan::ColLayout& C) {
     stats_.device_bytes = static_cast<long long>(C.blocks.size() + 4 * C.cta.size() + 4 * C.bidx.size() +
                                                  4 * C.wpos.size() + 16 * C.mailboxes);
     if (std::getenv("HEC_DEBUG"))
-        std::fprintf(stderr, "[hec] columns n=%d grid=%dx%dx%d tiles=%dx%d warps=%dx%d ctas=%d slots=%lld levels=%lld "
+        std::fprintf(stderr, "[hec] columns n=%d grid=%dx%dx%d tiles=%dx%d warps=%dx%d rpl=%d ctas=%d slots=%lld levels=%lld "
                      "ring=%d block=%d unit=%d mirrored=%d order=%d,%d,%d\n", C.n, C.nx, C.ny, C.nz, C.PX, C.PY, C.WX,
-                     C.WY, C.ctas, C.slots, C.total_levels, C.ring, C.block_bytes, C.unit ? 1 : 0, C.mirrored ? 1 : 0,
+                     C.WY, C.rpl, C.ctas, C.slots, C.total_levels, C.ring, C.block_bytes, C.unit ? 1 : 0, C.mirrored ? 1 : 0,
                      C.order & 3, (C.order >> 2) & 3, (C.order >> 4) & 3);
     spare_ = make_workspace();
 }
@@ -308,7 +309,7 @@ void DeviceTri::launch_cols(const double* bp, double* xw, cudaStream_t st, unsig
     a.PY = c_info_.PY;
     a.ox = c_info_.ox;
     a.oy = c_info_.oy;
-    a.mbox_top0 = static_cast<long long>(p_ctas_) * (4 * a.WY) * a.nz;
+    a.mbox_top0 = static_cast<long long>(p_ctas_) * (4 * c_info_.rpl * a.WY) * a.nz;
     a.block_bytes = c_block_bytes_;
     a.ring = c_ring_;
     a.bp_reversed = mirrored_ ? 1 : 0;
@@ -316,7 +317,7 @@ void DeviceTri::launch_cols(const double* bp, double* xw, cudaStream_t st, unsig
     a.order = c_info_.order;
     a.trace = trace;
     void* args[] = {&a};
-    HEC_CUDA(cudaLaunchCooperativeKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_), dim3(32 * c_warps_),
+    HEC_CUDA(cudaLaunchCooperativeKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_), dim3(32 * (c_warps_ + 1)),
                                          args, p_smem_, st));
 }
 

@@ -66,7 +66,7 @@ struct ColArgs {
     unsigned long long watchdog_cycles;
     unsigned long long* trace;    // diagnostics (trace kernel): 4 words per CTA level (warp 0, lane 0)
 };
-void* cols_kernel(int warps, bool unit, bool trace, int order);
+void* cols_kernel(int warps, int rpl, bool unit, bool trace, int order);
 constexpr int kColOrderZYX = 2 | 1 << 2 | 0 << 4;  // (z-1, y-1, x-1): natural-order 7-point factors
 
 // one launch per level, arguments read from dev_args (capturable once, replayed for any vectors)

@@ -972,9 +972,12 @@ ColLayout build_columns(const TriSource& s, const ColConfig& cfg) {
     P.nlev = nx + ny + nz - 2;
     P.unit = nonunit == 0;
     P.order = order[0] | order[1] << 2 | order[2] << 4;
-    constexpr int SX = ColLayout::SX, SY = ColLayout::SY;
+    constexpr int SX = ColLayout::SX;
+    int SY = 4;
     if (cfg.mirror) {
         const ColMirror& m = *cfg.mirror;
+        P.rpl = m.rpl;
+        SY = 4 * P.rpl;
         if (m.nx != nx || m.ny != ny || m.nz != nz || !s.reversed) throw std::invalid_argument("columns: no mirror");
         P.WX = m.WX;
         P.WY = m.WY;
@@ -984,32 +987,44 @@ ColLayout build_columns(const TriSource& s, const ColConfig& cfg) {
         P.oy = m.PY * SY * m.WY - ny - m.oy;
         P.mirrored = true;
     } else {
-        // tiling: one CTA per SM at most; the level chain costs ~max(300, 0.6 * lanes)
-        // cycles a level, each CTA boundary a wavefront crosses ~2000 cycles of lag
+        // tiling: one CTA per SM at most. A level costs a warp ~250 cycles of
+        // latency, and the SM has to stream the CTA's row data (~41 bytes a column,
+        // ~60 bytes / cycle); each CTA boundary a wavefront crosses adds ~2000
+        // cycles of lag
+        // shapes (warps, columns per lane): one lane-column per level costs ~20 cycles of a
+        // warp's dependent instruction chain, a level ~150 more; each CTA boundary a
+        // wavefront crosses adds ~2000 cycles of lag; the SM streams ~41 bytes a column
+        // (~60 bytes / cycle)
         double best = 1e300;
-        for (int nw : {16, 8, 4, 2, 1}) {
+        const int shapes[][2] = {{16, 1}, {8, 2}, {4, 4}, {4, 1}, {1, 4}};
+        for (const auto& sh : shapes) {
+            const int nw = sh[0], rp = sh[1];
             if (cfg.warps > 0 && nw != cfg.warps) continue;
+            if (cfg.rpl > 0 && rp != cfg.rpl) continue;
             for (int wx = 1; wx <= nw; wx *= 2) {
                 const int wy = nw / wx;
-                const int tx = SX * wx, ty = SY * wy;
+                const int tx = SX * wx, ty = 4 * rp * wy;
                 const int px = (nx + tx - 1) / tx, py = (ny + ty - 1) / ty;
                 if (static_cast<long long>(px) * py > cfg.ctas) continue;
-                const double est = P.nlev * std::max(300.0, 0.6 * 32 * nw) + 2000.0 * (px + py - 2);
+                const double per_level = std::max({150.0 + 80.0 * rp, 41.0 * tx * ty / 60.0});
+                const double est = P.nlev * per_level + 2000.0 * (px + py - 2);
                 if (est < best) {
                     best = est;
                     P.WX = wx;
                     P.WY = wy;
                     P.PX = px;
                     P.PY = py;
+                    P.rpl = rp;
                 }
             }
         }
+        SY = 4 * P.rpl;
         if (best >= 1e300) throw std::invalid_argument("columns: no tiling fits the CTA count");
     }
     const int TX = SX * P.WX, TY = SY * P.WY, C = P.PX * P.PY;
     P.ctas = C;
     P.warps = P.WX * P.WY;
-    P.lanes = 32 * P.warps;
+    P.lanes = 32 * P.rpl * P.warps;  // slots per level
     const int NS = P.lanes;
     P.block_bytes = round_up((P.unit ? 24 : 40) * NS + NS, 16);
     const int per_level = P.block_bytes + 8 * NS;
@@ -1057,7 +1072,8 @@ ColLayout build_columns(const TriSource& s, const ColConfig& cfg) {
         const int ax = x + P.ox, ay = y + P.oy;
         const int px = ax / TX, py = ay / TY, c = py * P.PX + px;
         const int wx = (ax % TX) / SX, lx = ax % SX, wy = (ay % TY) / SY, ly = ay % SY;
-        const int k = (wy * P.WX + wx) * 32 + ly * SX + lx;
+        // lane (ly / RPL) * SX + lx owns RPL consecutive columns in y; its slots are consecutive
+        const int k = ((wy * P.WX + wx) * 32 + (ly / P.rpl) * SX + lx) * P.rpl + ly % P.rpl;
         const int l = x + y + z - P.cta[4 * c];
         const long long sl = static_cast<long long>(P.cta[4 * c + 2]) * NS + static_cast<long long>(l) * NS + k;
         unsigned char* q = P.blocks.data() + (static_cast<std::size_t>(P.cta[4 * c + 3]) + l) * P.block_bytes;

@@ -210,41 +210,47 @@ inline WaveSections wave_sections(int m, int w, int nw, int nhalo, int ntail, in
 // (every dependency of row (x,y,z) is one of (x-1,y,z), (x,y-1,z), (x,y,z-1),
 // in any ELL/CSR order): row (x,y,z) sits on level x+y+z, and along a grid
 // column (x,y) the rows follow one another level by level. Each solver lane
-// then owns one column for the whole solve and keeps that column's latest x in
-// a register: at level L it needs exactly the latest values of its own column
-// (z-1), of column (x-1,y) and of column (x,y-1) -- a register, two warp
-// shuffles, and at warp / CTA tile edges a shared-memory edge buffer or an
+// then owns four columns for the whole solve and keeps their latest x in
+// registers: at level L, row (x,y,z) needs exactly the latest values of its own
+// column (z-1), of column (x-1,y) and of column (x,y-1) -- registers, warp
+// shuffles, and at warp / CTA tile edges a shared-memory edge ring or an
 // epoch-tagged mailbox. No dependency indices, no x ring, no per-chunk blob
-// decode: per level and lane only the row's values, the entry order code and
-// b are read (one TMA bulk copy per CTA level into a shared-memory ring).
+// decode: per level and lane only the rows' values, their presence mask and b
+// are read (one TMA bulk copy per CTA level into a shared-memory ring). The
+// warps of a CTA run free: each waits only for its left and lower neighbour
+// warps' previous level (shared-memory progress counters).
 //
-// CTA (px, py) owns a TX x TY tile of columns, TX = 8 WX, TY = 4 WY; warp
-// (wx, wy) owns an 8 x 4 sub-tile, lane = ly * 8 + lx. Column
-// x = px*TX + wx*8 + lx - ox (and y likewise); ox, oy anchor the tiling
-// (0, or at the far end for the mirror of another layout). Slots: CTA-major,
-// then the CTA's levels, then 32*NW lanes per level (lanes whose column is off
-// the grid or whose row is outside [0, nz) are padding). The right-hand side
-// is permuted into slot order (bidx), x comes out in slot order (wpos).
+// CTA (px, py) owns a TX x TY tile of columns, TX = 8 WX, TY = 4 rpl WY; warp
+// (wx, wy) owns an 8 x 4 rpl sub-tile, lane lq * 8 + lx owns the columns
+// (lx, rpl lq .. rpl lq + rpl - 1) of it (rpl = 1, 2 or 4 columns per lane). Column x = px*TX + wx*8 + lx - ox (y likewise);
+// ox, oy anchor the tiling (0, or at the far end for the mirror of another
+// layout). Slots: CTA-major, then the CTA's levels, then 32*rpl*NW per level
+// ((warp * 32 + lane) * rpl + r; columns off the grid and rows outside [0, nz)
+// are padding). The right-hand side is permuted into slot order (bidx), x
+// comes out in slot order (wpos).
 // shared memory in front of the level ring: full[16] / empty[16] mbarriers, then
-// the warp edge buffers (2 parities x 16 warps x (4 + 8) doubles)
-constexpr int kColCtrlBytes = 4096;
+// the warp edge rings (12 levels x (64 + 128) tagged values of 16 bytes)
+constexpr int kColEdgeLevels = 12;
+constexpr int kColCtrlBytes = 256 + kColEdgeLevels * 192 * 16;
 struct ColMirror {
     int nx = 0, ny = 0, nz = 0, WX = 0, WY = 0, PX = 0, PY = 0, ox = 0, oy = 0;
     long long slots = 0;
-    int order = 0;
+    int order = 0, rpl = 1;
 };
 struct ColConfig {
     int ctas = 148;
     int warps = 0;                       // solver warps per CTA (WX*WY); 0 = chosen here
+    int rpl = 0;                         // columns per lane; 0 = chosen here
     int smem_bytes = 0;                  // dynamic shared memory budget (level ring)
-    int ring_max = 16;                   // level blocks in flight at most (<= 16)
+    int ring_max = kColEdgeLevels - 2;   // level blocks in flight at most (the edge rings hold kColEdgeLevels)
     const ColMirror* mirror = nullptr;   // build the exact mirror of this layout (U of an ILU pair)
 };
 struct ColLayout {
-    static constexpr int SX = 8, SY = 4;
+    static constexpr int SX = 8;         // warp sub-tile 8 x 4 rpl: lane (lq, lx) owns y = rpl lq .. rpl lq + rpl - 1
+    int rpl = 1;                         // columns per lane (1, 2 or 4)
     int n = 0, nx = 0, ny = 0, nz = 0;
     int WX = 1, WY = 1, PX = 1, PY = 1, ox = 0, oy = 0;
-    int ctas = 0, warps = 0, lanes = 0;  // lanes = 32 * warps slots per level
+    int ctas = 0, warps = 0, lanes = 0;  // lanes = 32 * rpl * warps slots per level
     int nlev = 0;                        // nx + ny + nz - 2 levels of the grid
     int block_bytes = 0;                 // one CTA level: val[3][lanes] f64 (by position in `order`),
                                          //   (diag, rcp)[lanes] f64 unless unit, mask[lanes] u8 (present positions)
@@ -260,7 +266,7 @@ struct ColLayout {
     std::vector<int> bidx;               // S: input index of the row in each slot (0 for padding)
     std::vector<int> wpos;               // n: solution index -> slot
     ColMirror mirror_info() const {
-        return ColMirror{nx, ny, nz, WX, WY, PX, PY, ox, oy, slots, order};
+        return ColMirror{nx, ny, nz, WX, WY, PX, PY, ox, oy, slots, order, rpl};
     }
 };
 // Throws std::invalid_argument when the factor is not such a grid (or carries

@@ -31,11 +31,13 @@ def _want(orc, f, b):
     return y, orc.solve(orc.prepare(to_oracle(f.u), upper=True), y)
 
 
-@pytest.mark.parametrize("warps", ["", "1", "2", "4", "16"])
+@pytest.mark.parametrize("shape", ["", "16x1", "8x2", "4x4", "4x1", "1x4"])  # warps x columns per lane
 @pytest.mark.parametrize("dims", GRIDS)
-def test_columns_bitwise(H, orc, monkeypatch, dims, warps):
-    if warps:
+def test_columns_bitwise(H, orc, monkeypatch, dims, shape):
+    warps = shape.split("x")[0] if shape else ""
+    if shape:
         monkeypatch.setenv("HEC_COLS_WARPS", warps)
+        monkeypatch.setenv("HEC_COLS_RPL", shape.split("x")[1])
     a, f = _factors(H, dims, seed=7)
     rng = np.random.default_rng(11)
     b = rng.uniform(-1, 1, a.n_rows)
@@ -43,8 +45,8 @@ def test_columns_bitwise(H, orc, monkeypatch, dims, warps):
     tl, tu = H.DeviceTri.create(H.prepare_lower(f.l)), H.DeviceTri.create(H.prepare_upper(f.u))
     il, iu = tl.info(), tu.info()
     assert il["layout"] == 4 and iu["layout"] == 4, (il, iu)
-    if warps:
-        assert il["group"] == int(warps)
+    if shape:
+        assert (il["group"], il["rows_per_lane"]) == tuple(int(v) for v in shape.split("x")), il
     assert il["wave_len"] >= a.n_rows
     assert bits_equal(tl.solve_host(b), y_want), "L"
     assert bits_equal(tu.solve_host(y_want), x_want), "U"

@@ -52,13 +52,12 @@ def main():
     print(f"per-level period (median per CTA) p10 {np.percentile(per, 10):.0f} p50 {np.median(per):.0f} "
           f"p90 {np.percentile(per, 90):.0f} ns; level start->end p50 {np.median(busy):.0f} ns")
     ld = loaded - start
-    print(f"warp 0: level start -> next level's data loaded p50 {np.median(ld[start > 0]):.0f} ns, "
-          f"loaded -> barrier passed p50 {np.median((end - loaded)[start > 0]):.0f} ns")
     st = tr[:, 4:8]
     ok = st[:, 3] > 0
     ok[c0[1]:] = False  # CTA 0 only: no mailbox waits
-    print("warp 0 SM-clock stamps from level start (cycles, p50): neighbours " + ", ".join(
-        f"{n} {np.median(st[ok, i]):.0f}" for i, n in enumerate(("values", "x", "stores+arrive", "next loaded"))))
+    if ok.any(): print("warp 0 SM-clock stamps from level start (cycles, p50): " + ", ".join(
+        f"{n} {np.median(st[ok, i]):.0f}" for i, n in enumerate(("data ready", "data loaded", "x", "published"))) +
+        f", level end {np.median(tr[ok, 2]):.0f}")
     print(f"mailbox re-polls per CTA: p50 {np.median(polls):.0f} max {max(polls)}; total {sum(polls)}")
     order = np.argsort(first)
     for c in order[:: max(1, ncta // 12)]:
