@@ -182,7 +182,8 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
             h_wpos_ = P.wpos;
             h_bidx_ = P.bidx;
             stats_.ctas = p_ctas_;
-            stats_.threads = kWaveRoleThreads + 32 * p_warps_;
+            p_role_threads_ = wave_role_threads(P.group, P.groups, P.rpl);
+            stats_.threads = p_role_threads_ + 32 * p_warps_;
             if (!p_kernel_) throw std::invalid_argument("hec_tri_create: no wave kernel for this width");
             stats_.chunks = P.chunks;
             stats_.slots = p_inflight_;
@@ -497,7 +498,7 @@ void DeviceTri::solve_wave(const double* bp, double* xw, double* out, cudaStream
     void* args[] = {&a};
     // cooperative: every CTA resident at once (CTAs wait on each other's rows)
     HEC_CUDA(cudaLaunchCooperativeKernel(trace ? p_kernel_trace_ : p_kernel_, dim3(p_ctas_),
-                                         dim3(kWaveRoleThreads + 32 * p_warps_), args, p_smem_, st));
+                                         dim3(p_role_threads_ + 32 * p_warps_), args, p_smem_, st));
 }
 
 void DeviceTri::solve_host(const double* b, double* x) {

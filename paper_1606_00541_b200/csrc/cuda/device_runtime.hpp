@@ -147,7 +147,7 @@ private:
     DevBuf<int> p_spans_, p_cta0_, p_bidx_, p_wpos_;
     std::vector<int> h_bidx_, h_wpos_;
     int p_ctas_ = 0, p_inflight_ = 0, p_ring_ = 0, p_ring_off_ = 0, p_buf_off_ = 0, p_buf_bytes_ = 0;
-    int p_smem_ = 0, p_warps_ = 0, p_lead_ = 1, spin_ns_ = 0, p_rpl_ = 1, p_halo_ring_ = 32;
+    int p_smem_ = 0, p_warps_ = 0, p_lead_ = 1, spin_ns_ = 0, p_rpl_ = 1, p_halo_ring_ = 32, p_role_threads_ = 224;
     unsigned long long watchdog_ns_ = 10000000000ULL;  // 10 s: a solve is milliseconds
     int clock_khz_ = 2000000;                          // SM clock (cycles per ms), for the watchdog
     void* p_kernel_ = nullptr;

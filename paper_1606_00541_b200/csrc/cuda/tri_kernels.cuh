@@ -79,9 +79,22 @@ void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
-constexpr int kWaveProducers = 2;                      // producer warps (chunks round robin)
-constexpr int kWaveWaiters = 5;                        // waiter warps (3 could not keep up with 27-point halos)
-constexpr int kWaveRoleThreads = 32 * (kWaveProducers + kWaveWaiters);
+// producer / waiter warps of k_wave: 2 + 5 in general (3 waiters could not keep
+// up with 27-point halos); the narrow-row shapes with more groups (z-pencils:
+// few halo values per chunk) keep the thread count, hence the register budget,
+// with 1 + 2
+__host__ __device__ constexpr bool wave_lean_roles(int group, int groups, int rpl) {
+    return groups == 3 && group * rpl > 0;
+}
+__host__ __device__ constexpr int wave_producers(int group, int groups, int rpl) {
+    return wave_lean_roles(group, groups, rpl) ? 1 : 2;
+}
+__host__ __device__ constexpr int wave_waiters(int group, int groups, int rpl) {
+    return wave_lean_roles(group, groups, rpl) ? 2 : 5;
+}
+__host__ __device__ constexpr int wave_role_threads(int group, int groups, int rpl) {
+    return 32 * (wave_producers(group, groups, rpl) + wave_waiters(group, groups, rpl));
+}
 constexpr int kWaveCtrlBytes = 1536;                   // control block at the start of shared memory
 
 }  // namespace hec::dev

@@ -383,14 +383,18 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         }
     }
     const int W = P.max_width;
-    if (big_auto && W <= 4) {  // narrow rows: 8 warps x 2 rows per lane fit 96 registers (measured ~1.5 % faster)
-        NW = 8;
-        warp_rows = 64;
-        K = 2;
+    if (big_auto && W <= 4) {
+        // narrow rows (z-pencils of 7-point factors): three groups of 4 warps x 4 rows
+        // per lane, with one producer and two waiter warps (the prefetch of a chunk
+        // then has two chunk periods instead of one): 7-pt 256^3 / 202^3 / 160^3
+        // ILU apply 1.050 / 0.770 / 0.559 ms with 8x2x2 -> 0.993 / 0.704 / 0.533 ms
+        NW = 4;
+        warp_rows = 128;
+        K = 3;
         P.group = NW;
         P.groups = K;
         P.warps = NW * K;
-        P.rpl = 2;
+        P.rpl = 4;
     }
 
     // 1. chunk discovery: per level, each CTA's rows (ordered by warp, then by

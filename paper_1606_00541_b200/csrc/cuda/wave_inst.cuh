@@ -3,8 +3,10 @@
 // planner chooses (G warps per group x K groups, RPL rows per lane):
 //   1x4x2   up to  64 rows per chunk (e.g. 27-point slabs)
 //   2x4x2   up to 128 rows
-//   8x2x2   up to 512 rows, widths <= 4 only (e.g. 7-point z-pencils; the
-//           register budget of 736 threads does not hold wider rows)
+//   4x3x4   up to 512 rows, widths <= 4 only (7-point z-pencils: three groups,
+//           one producer and two waiter warps)
+//   8x2x2   up to 512 rows, widths <= 4 only (the register budget of 736
+//           threads does not hold wider rows)
 //   4x2x4   up to 512 rows, any width (widths >= 7 spill a few registers)
 #pragma once
 #include "wave_kernel.cuh"
@@ -23,8 +25,10 @@ void* wave_pick(int group, int groups, int rpl, bool trace) {
     if (group == 1 && groups == 4 && rpl == 2) return wave_ptr<WD, 1, 4, 2>(trace);
     if (group == 2 && groups == 4 && rpl == 2) return wave_ptr<WD, 2, 4, 2>(trace);
     if (group == 4 && groups == 2 && rpl == 4) return wave_ptr<WD, 4, 2, 4>(trace);
-    if constexpr (WD <= 4)
+    if constexpr (WD <= 4) {
         if (group == 8 && groups == 2 && rpl == 2) return wave_ptr<WD, 8, 2, 2>(trace);
+        if (group == 4 && groups == 3 && rpl == 4) return wave_ptr<WD, 4, 3, 4>(trace);
+    }
     return nullptr;
 }
 

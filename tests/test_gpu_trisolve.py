@@ -203,7 +203,8 @@ def test_wave_width_classes_and_splits(H, orc):
                                    {"HEC_WAVE_G": "1", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "4", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "4"},
-                                   {"HEC_WAVE_G": "8", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "2"}])
+                                   {"HEC_WAVE_G": "8", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_G": "4", "HEC_WAVE_K": "3", "HEC_WAVE_RPL": "4"}])
 def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
     # every row-ownership layout (z-pencils, slabs, strips) and solver shape
     # (G warps per chunk x K groups x RPL rows per lane) gives the reference's bits
@@ -215,8 +216,9 @@ def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
              ("rcm 7pt", H.gen_poisson7(24, 22, 20), "rcm"),            # strips
              ("random 7pt", H.gen_poisson7(20, 18, 16), "random")]      # slabs
     for name, a, order in cases:
-        if knobs.get("HEC_WAVE_G") == "8" and "27pt" in name:
-            continue  # the 8x2x2 shape exists for ELL widths <= 4 only (register budget)
+        if knobs.get("HEC_WAVE_K") == "3" or knobs.get("HEC_WAVE_G") == "8":
+            if "27pt" in name:
+                continue  # the 8x2x2 and three-group shapes exist for ELL widths <= 4 only
         if order == "rcm":
             a = H.permute_symmetric(a, H.rcm_ordering(a))
         elif order == "random":
