@@ -38,7 +38,7 @@ def main():
     tr, c0 = t.solve_traced(b, x)
     tr = tr.astype(np.int64)
     info = t.info()
-    nw = info["threads"] // 32 - 7
+    nw = info["group"] * info["groups"]  # solver warps
     T0 = tr[:, 0][tr[:, 0] > 0].min()
     T = np.where(tr > 0, tr - T0, -1)
     issued, landed, ready = T[:, 0], T[:, 1], T[:, 3]
