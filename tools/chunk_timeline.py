@@ -43,7 +43,7 @@ def main():
     tr, c0 = t.solve_traced(b, x)
     tr = tr.astype(np.int64)
     info = t.info()
-    nw = info["threads"] // 32 - 7  # 2 producer + 5 waiter warps
+    nw = info["group"] * info["groups"]  # solver warps (role warps vary with the shape)
     T = np.where(tr > 0, tr - tr[:, 0].min(), -1)
     c = args.cta if args.cta >= 0 else (len(c0) - 1) // 2
     lo, hi = c0[c], c0[c + 1]

@@ -27,7 +27,7 @@ def main():
     tr, c0 = t.solve_traced(b, x)
     tr = tr.astype(np.int64)
     info = t.info()
-    nw = info["threads"] // 32 - 7
+    nw = info["group"] * info["groups"]  # solver warps
     T = np.where(tr > 0, tr - tr[:, 0].min(), -1)
     done = T[:, 10:10 + 3 * nw:3].max(axis=1)
     C = len(c0) - 1

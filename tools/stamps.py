@@ -45,7 +45,7 @@ def main():
     ok = cyc[:, 5] > 0
     med = np.median(cyc[ok], axis=0)
     T = np.where(tr > 0, tr - tr[:, 0].min(), -1)
-    nw = info["threads"] // 32 - 7  # 2 producer + 5 waiter warps
+    nw = info["group"] * info["groups"]  # solver warps (role warps vary with the shape)
     dd, dn = T[:, 9:9 + 3 * nw:3], T[:, 10:10 + 3 * nw:3]
     last = dn.max(axis=1)
     cm = (len(c0) - 1) // 2

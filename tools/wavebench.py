@@ -85,7 +85,7 @@ def main():
         if args.trace:
             tr, c0 = t.solve_traced(b, x)
             tr = tr.astype(np.int64)
-            nw = info["threads"] // 32 - 7
+            nw = info["group"] * info["groups"]  # solver warps
             T = np.where(tr > 0, tr - tr[:, 0].min(), -1)
             rs, dd, dn = T[:, 8:8 + 3 * nw:3], T[:, 9:9 + 3 * nw:3], T[:, 10:10 + 3 * nw:3]
             pct = lambda a: "p10 %.0f p50 %.0f p90 %.0f" % tuple(np.percentile(a, [10, 50, 90]))
