@@ -1,8 +1,10 @@
 // Instantiation of k_wave for a set of sliced-ELL widths (one translation unit
 // per width group, so the widths compile in parallel). Solver shapes the
 // planner chooses (G warps per group x K groups, RPL rows per lane):
-//   1x4x2   up to  64 rows per chunk (e.g. 27-point slabs)
-//   2x4x2   up to 128 rows
+//   2x4x1   up to  64 rows per chunk (e.g. 27-point slabs; one row per lane: 27-pt
+//           128^3 ILU apply 0.946 -> 0.922 ms against 1x4x2)
+//   4x4x1   up to 128 rows (7-pt 128^3 0.277 -> 0.264 ms against 2x4x2)
+//   1x4x2, 2x4x2   the same capacities with two rows per lane
 //   4x3x4   up to 512 rows, widths <= 4 only (7-point z-pencils: three groups,
 //           one producer and two waiter warps)
 //   8x2x2   up to 512 rows, widths <= 4 only (the register budget of 736
@@ -24,6 +26,8 @@ template <int WD>
 void* wave_pick(int group, int groups, int rpl, bool trace) {
     if (group == 1 && groups == 4 && rpl == 2) return wave_ptr<WD, 1, 4, 2>(trace);
     if (group == 2 && groups == 4 && rpl == 2) return wave_ptr<WD, 2, 4, 2>(trace);
+    if (group == 2 && groups == 4 && rpl == 1) return wave_ptr<WD, 2, 4, 1>(trace);
+    if (group == 4 && groups == 4 && rpl == 1) return wave_ptr<WD, 4, 4, 1>(trace);
     if (group == 4 && groups == 2 && rpl == 4) return wave_ptr<WD, 4, 2, 4>(trace);
     if constexpr (WD <= 4) {
         if (group == 8 && groups == 2 && rpl == 2) return wave_ptr<WD, 8, 2, 2>(trace);

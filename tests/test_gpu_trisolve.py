@@ -202,6 +202,8 @@ def test_wave_width_classes_and_splits(H, orc):
 @pytest.mark.parametrize("knobs", [{}, {"HEC_WAVE_SLABS": "1"},
                                    {"HEC_WAVE_G": "1", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
+                                   {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "1"},
+                                   {"HEC_WAVE_G": "4", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "1"},
                                    {"HEC_WAVE_G": "4", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "4"},
                                    {"HEC_WAVE_G": "8", "HEC_WAVE_K": "2", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "4", "HEC_WAVE_K": "3", "HEC_WAVE_RPL": "4"}])
