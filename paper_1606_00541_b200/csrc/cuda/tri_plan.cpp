@@ -576,9 +576,14 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         };
         // a small x ring leaves room for a larger halo ring (27-point slabs: NS 8 -> 16, -3 %)
         const int hmax = R <= 2048 ? 2 * cfg.halo_ring_max : cfg.halo_ring_max;
-        int ns = P.inflight;
+        // at least two descriptor slots per solver group: with NS == K (a group
+        // always refilling its own slot) the kernel deadlocks -- measured with
+        // HEC_WAVE_INFLIGHT=4 and four groups, caught by the watchdog
+        int ns_min = 4;
+        while (ns_min < 2 * P.groups) ns_min *= 2;
+        int ns = std::max(P.inflight, ns_min);
         int need = need_for(ns);
-        while (need > hmax && ns > 4) need = need_for(ns /= 2);  // NS >= 4 (kernel slot waits)
+        while (need > hmax && ns > ns_min) need = need_for(ns /= 2);
         if (need > hmax)
             throw std::invalid_argument("hec_tri_create: halo ring overflow (wave layout)");
         P.inflight = ns;

@@ -200,6 +200,7 @@ def test_wave_width_classes_and_splits(H, orc):
 
 
 @pytest.mark.parametrize("knobs", [{}, {"HEC_WAVE_SLABS": "1"},
+                                   {"HEC_WAVE_INFLIGHT": "4"},  # the planner keeps >= 2 slots per group
                                    {"HEC_WAVE_G": "1", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "2"},
                                    {"HEC_WAVE_G": "2", "HEC_WAVE_K": "4", "HEC_WAVE_RPL": "1"},
