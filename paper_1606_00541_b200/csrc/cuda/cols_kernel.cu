@@ -26,30 +26,6 @@ namespace {
 
 constexpr int kEdge = plan::kColEdgeLevels;  // levels in the warp edge rings (> slot ring depth + 1)
 
-__device__ __noinline__ double mail_late(const unsigned long long* p, int ahead, uint32_t ep, uint64_t deadline,
-                                         uint32_t& polls) {
-    ulonglong2 w = ld_relaxed_v2(p + 2 * ahead);
-    while (!mail_ok(w, ep)) {
-        watchdog(polls, deadline);
-        w = ld_relaxed_v2(p + 2 * ahead);
-    }
-    ulonglong2 v = ld_relaxed_v2(p);
-    while (!mail_ok(v, ep)) {  // rows of a column are produced in order, but may be seen out of order
-        watchdog(polls, deadline);
-        v = ld_relaxed_v2(p);
-    }
-    return mail_value(v);
-}
-// The value of row z from a neighbouring CTA's mailbox p (v: loaded a few levels
-// ago). If it was not produced yet this CTA has caught up with its neighbour: it
-// then waits until the neighbour is `ahead` rows further down the column.
-__device__ __forceinline__ double mail_get(ulonglong2 v, const unsigned long long* p, int ahead, uint32_t ep,
-                                           uint64_t deadline, uint32_t& polls) {
-    if (__builtin_expect(mail_ok(v, ep), 1)) return mail_value(v);
-    ++polls;
-    return mail_late(p, ahead, ep, deadline, polls);
-}
-
 // Warp edge rings in shared memory carry each value as two 8-byte words
 // {lo32 | tag << 32, hi32 | tag << 32} (tag = level + 1): every word is written
 // atomically, so a reader polls until both words carry the level it needs -- no
@@ -62,13 +38,6 @@ __device__ __forceinline__ void edge_put(ulonglong2* e, double x, uint32_t tag) 
     asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_u32(e)), "l"((bits & 0xffffffffULL) | t),
                  "l"((bits >> 32) | t)
                  : "memory");
-}
-__device__ __forceinline__ double edge_get(const ulonglong2* e, uint32_t tag) {
-    unsigned long long lo, hi;
-    do {
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(smem_u32(e)) : "memory");
-    } while (static_cast<uint32_t>(lo >> 32) != tag || static_cast<uint32_t>(hi >> 32) != tag);
-    return __longlong_as_double(static_cast<long long>((hi << 32) | (lo & 0xffffffffULL)));
 }
 __device__ __forceinline__ ulonglong2 lds_v2(const ulonglong2* e) {
     ulonglong2 v;
@@ -83,7 +52,11 @@ __device__ __noinline__ ulonglong2 edge_wait(const ulonglong2* e, uint32_t tag) 
     } while (!mail_ok(v, tag));
     return v;
 }
-// mail_late returning the mailbox words (for the vote path)
+// A neighbouring CTA's mailbox p that was not produced yet when it was loaded
+// early: this CTA has caught up with its neighbour, so it waits until the
+// neighbour is `ahead` rows further down the column (later early loads then
+// find their rows ready), then re-polls row z itself (rows of a column are
+// produced in order but may be seen out of order). Returns the mailbox words.
 __device__ __noinline__ ulonglong2 mail_late2(const unsigned long long* p, int ahead, uint32_t ep, uint64_t deadline,
                                               uint32_t& polls) {
     ++polls;
