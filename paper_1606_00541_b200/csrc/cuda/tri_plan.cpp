@@ -86,11 +86,95 @@ GridGeom detect_grid(const TriSource& s) {
     return g;
 }
 
+// Grid coordinates from the dependency DAG, for orderings other than the natural
+// one that still orient every grid edge towards increasing coordinates (reverse
+// Cuthill-McKee started at a corner, and other orderings that grow from a
+// corner): the factor of a 7-point stencil then has a single source (the
+// corner); a row with one predecessor continues its predecessor's axis line
+// (the corner's successors open the three axes); a row with two or three
+// predecessors sits at their component-wise maximum. Checked: every dependency
+// is a unit step from the previous level and the coordinates fill an X x Y x Z
+// box exactly once -- anything else returns false. cx, cy: x and y of every
+// lower-frame row.
+bool dag_grid(const TriSource& s, std::vector<int>& cx, std::vector<int>& cy, GridGeom& g) {
+    const int n = s.n;
+    if (n < 4096) return false;
+    std::vector<int> lev(n);
+    for (int k = 0; k < s.nlev; ++k)
+        for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r) lev[s.inv_perm[r]] = k;
+    std::vector<int> co(3 * static_cast<std::size_t>(n), 0);
+    std::vector<signed char> axis(n, -1);
+    int next_axis = 0;
+    for (int r = 0; r < n; ++r) {  // level-major: every predecessor comes first
+        const int i = s.inv_perm[r];
+        int pr[4], np = 0;
+        for_each_entry(s, r, [&](int col, double) {
+            if (np < 4) pr[np] = s.inv_perm[col];
+            ++np;
+        });
+        int* c = &co[3 * static_cast<std::size_t>(i)];
+        if (np > 3) return false;
+        if (np == 0) {
+            if (r != 0) return false;  // one source only
+            continue;
+        }
+        for (int k = 0; k < np; ++k)
+            if (lev[pr[k]] != lev[i] - 1) return false;
+        if (np == 1) {
+            const int p = pr[0];
+            int a;
+            if (lev[p] == 0) {
+                if (next_axis >= 3) return false;
+                a = next_axis++;
+            } else {
+                a = axis[p];
+                if (a < 0) return false;
+            }
+            for (int d = 0; d < 3; ++d) c[d] = co[3 * static_cast<std::size_t>(p) + d];
+            c[a] += 1;
+            axis[i] = static_cast<signed char>(a);
+            continue;
+        }
+        for (int d = 0; d < 3; ++d) {
+            int m = 0;
+            for (int k = 0; k < np; ++k) m = std::max(m, co[3 * static_cast<std::size_t>(pr[k]) + d]);
+            c[d] = m;
+        }
+        for (int k = 0; k < np; ++k) {  // a unit step from every predecessor
+            int diff = 0;
+            for (int d = 0; d < 3; ++d) diff += c[d] - co[3 * static_cast<std::size_t>(pr[k]) + d];
+            if (diff != 1) return false;
+        }
+    }
+    int ext[3] = {0, 0, 0};
+    for (int i = 0; i < n; ++i)
+        for (int d = 0; d < 3; ++d) ext[d] = std::max(ext[d], co[3 * static_cast<std::size_t>(i) + d] + 1);
+    if (static_cast<long long>(ext[0]) * ext[1] * ext[2] != n) return false;
+    std::vector<unsigned char> seen(n, 0);
+    for (int i = 0; i < n; ++i) {
+        const int* c = &co[3 * static_cast<std::size_t>(i)];
+        const long long at = c[0] + static_cast<long long>(ext[0]) * (c[1] + static_cast<long long>(ext[1]) * c[2]);
+        if (seen[at]++) return false;
+    }
+    cx.resize(n);
+    cy.resize(n);
+    for (int i = 0; i < n; ++i) {
+        cx[i] = co[3 * static_cast<std::size_t>(i)];
+        cy[i] = co[3 * static_cast<std::size_t>(i) + 1];
+    }
+    g.nx = ext[0];
+    g.ny = ext[1];
+    g.nz = ext[2];
+    g.ok = g.nx >= 4 && g.ny >= 4 && g.nz >= 2;
+    return g.ok;
+}
+
 // CTA tiles of (4 sx) x (4 sy) columns in x-y, each split into 4 x 4 warp
 // sub-tiles of sx x sy <= 32 columns (so a level never gives a warp more than
-// 32 rows): the most CTAs that fit C, ties to square sub-tiles.
+// 32 rows): the most CTAs that fit C, ties to square sub-tiles. cx / cy: the
+// rows' grid coordinates when the ordering is not the natural one (else null).
 bool pencil_owners(const GridGeom& g, int n, int C, int NW, std::vector<int>& owner, std::vector<int>& warp,
-                   int& used) {
+                   int& used, const int* cx = nullptr, const int* cy = nullptr) {
     int best = -1, bsx = 0, bsy = 0, bpx = 0, bpy = 0;
     for (int sx = 1; sx <= 32; ++sx)
         for (int sy = 1; sx * sy <= 32; ++sy) {
@@ -109,7 +193,7 @@ bool pencil_owners(const GridGeom& g, int n, int C, int NW, std::vector<int>& ow
     const int tw = 4 * bsx, th = 4 * bsy;
 #pragma omp parallel for schedule(static)
     for (int i = 0; i < n; ++i) {
-        const int x = i % g.nx, y = (i / g.nx) % g.ny;
+        const int x = cx ? cx[i] : i % g.nx, y = cy ? cy[i] : (i / g.nx) % g.ny;
         const int px = x / tw, py = y / th;
         owner[i] = py * bpx + px;
         warp[i] = (((y - py * th) / bsy) * 4 + (x - px * tw) / bsx) * NW / 16;  // 4x4 sub-tiles -> NW warps
@@ -250,12 +334,24 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         return m;
     };
     bool use_pencils = false;
-    if (!M && geo.ok && pencil_owners(geo, n, C0, 16, owner_i, warp_i, C_used)) {
+    auto slab_levels = [&]() {
         const int per = (n + C0 - 1) / C0;
         std::vector<int> slab(n);
         for (int i = 0; i < n; ++i) slab[i] = std::min(i / per, C0 - 1);
-        use_pencils = max_levels_per_cta(owner_i, C_used) < max_levels_per_cta(slab, C0);
-    }
+        return max_levels_per_cta(slab, C0);
+    };
+    if (!M && geo.ok && pencil_owners(geo, n, C0, 16, owner_i, warp_i, C_used))
+        use_pencils = max_levels_per_cta(owner_i, C_used) < slab_levels();
+    // a renumbered grid (e.g. RCM): the index offsets say nothing, the dependency
+    // DAG still has the grid's shape -- take the coordinates from it
+    GridGeom geo_dag;
+    std::vector<int> dag_x, dag_y;
+    // DAG grid, against the strips such an ordering would get otherwise (every CTA
+    // walks every level there)
+    if (!use_pencils && cfg.pencils && !M && dag_grid(s, dag_x, dag_y, geo_dag) &&
+        pencil_owners(geo_dag, n, C0, 16, owner_i, warp_i, C_used, dag_x.data(), dag_y.data()))
+        use_pencils = max_levels_per_cta(owner_i, C_used) < std::min(s.nlev, slab_levels() * 8);
+    if (!use_pencils) geo_dag.ok = false;
     // strips: when the row index follows the levels (e.g. an RCM ordering), index
     // slabs would give each CTA only a handful of consecutive levels and the CTAs
     // would run one after another; then every CTA takes a fraction of every level
@@ -270,8 +366,8 @@ WaveLayout build_wave(const TriSource& s, const WaveConfig& cfg) {
         P.mirrored = true;
     } else if (use_pencils) {
         P.pencils = true;
-        P.grid_nx = geo.nx;
-        P.grid_ny = geo.ny;
+        P.grid_nx = geo_dag.ok ? geo_dag.nx : geo.nx;
+        P.grid_ny = geo_dag.ok ? geo_dag.ny : geo.ny;
     } else if (use_strips) {
         P.strips = true;
         for (int k = 0; k < s.nlev; ++k) {

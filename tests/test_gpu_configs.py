@@ -33,7 +33,7 @@ CASES = {
     "c1_p7_64": (7, 64, "natural", 1),
     "c2_p27_128": (27, 128, "natural", 0),
     "c4_p7_256": (7, 256, "natural", 1),
-    "c5_p7_100_rcm": (7, 100, "rcm", 2),
+    "c5_p7_100_rcm": (7, 100, "rcm", 1),  # z-pencils from the DAG's grid coordinates
     "c5_p7_100_random": (7, 100, "random", None),
 }
 

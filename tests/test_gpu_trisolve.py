@@ -216,7 +216,8 @@ def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
     rng = np.random.default_rng(23)
     cases = [("natural 7pt", H.gen_poisson7(28, 26, 24), None),          # pencils
              ("natural 27pt", H.gen_poisson27(18, 17, 16), None),       # slabs, 1 warp
-             ("rcm 7pt", H.gen_poisson7(24, 22, 20), "rcm"),            # strips
+             ("rcm 7pt", H.gen_poisson7(24, 22, 20), "rcm"),            # pencils (grid from the DAG)
+             ("rcm 27pt", H.gen_poisson27(16, 15, 14), "rcm"),          # not pencils
              ("random 7pt", H.gen_poisson7(20, 18, 16), "random")]      # slabs
     for name, a, order in cases:
         if knobs.get("HEC_WAVE_K") == "3" or knobs.get("HEC_WAVE_G") == "8":
@@ -234,6 +235,23 @@ def test_wave_layouts_bitwise(H, orc, knobs, monkeypatch):
             got, info = device_solve(H, p, b, 2)
             assert info["strategy"] == 2, name
             assert bits_equal(got, want), (name, upper, knobs)
+
+
+def test_renumbered_grid_layouts(H, orc):
+    # an RCM-renumbered 7-point grid keeps the grid's dependency DAG: the planner
+    # recovers the coordinates from it and lays the factor out as z-pencils; a
+    # 27-point one (more than three predecessors) does not
+    rng = np.random.default_rng(31)
+    for a, pencils in ((H.gen_poisson7(26, 24, 22), True), (H.gen_poisson27(16, 15, 14), False)):
+        a = H.permute_symmetric(a, H.rcm_ordering(a))
+        f = H.ilu0(a)
+        for fac, upper in ((f.l, False), (f.u, True)):
+            p = (H.prepare_upper if upper else H.prepare_lower)(fac)
+            b = rng.uniform(-1, 1, a.n_rows)
+            want = orc.solve(orc.prepare(to_oracle(fac), upper=upper), b)
+            got, info = device_solve(H, p, b, 2)
+            assert (info["layout"] == 1) == pencils, info
+            assert bits_equal(got, want)
 
 
 def test_cuda_graph_replay(H, orc):
