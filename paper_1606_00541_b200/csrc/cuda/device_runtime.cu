@@ -202,8 +202,15 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
         }
     }
     if (strategy_ == 1 && n_ > 0) {
-        plan::LevelLayout L = plan::build_levels(src);
+        int long_min = plan::kLongRowMin;
+        if (const char* e = std::getenv("HEC_LEVELS_LONG")) long_min = std::max(0, std::atoi(e));  // 0: no warp rows
+        plan::LevelLayout L = plan::build_levels(src, long_min);
+        long_starts_ = L.long_starts;
+        l_long_min_ = L.long_min;
+        if (!L.long_rows.empty()) l_long_rows_.upload(L.long_rows);
         level_starts_ = L.level_starts;
+        if (const char* e = std::getenv("HEC_LEVELS_PERSIST")) l_persist_ = std::atoi(e) != 0;
+        if (l_persist_) l_starts_.upload(L.level_starts);
         l_width_ = L.width;
         l_ld_ = L.ld;
         l_bidx_.upload(L.bidx);
@@ -219,7 +226,7 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
         l_tail_val_.upload(L.tail_val);
         stats_.device_bytes = static_cast<long long>(
             4 * (L.bidx.size() + L.xidx.size() + L.oidx.size() + L.ell_dep.size() + L.tail_rp.size() +
-                 L.tail_dep.size()) +
+                 L.tail_dep.size() + L.long_rows.size()) +
             8 * (L.ell_val.size() + L.diag.size() + L.tail_val.size()));
         stats_.threads = 256;
         wave_len_ = n_;
@@ -431,17 +438,25 @@ void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* ou
         a.tail_rp = l_tail_rp_.p;
         a.tail_dep = l_tail_dep_.p;
         a.tail_val = l_tail_val_.p;
+        a.long_rows = l_long_rows_.p;
+        a.long_min = l_long_min_;
         a.width = l_width_;
         a.ld = l_ld_;
         Workspace& w = workspace(st);
         LevelArgs* dev = reinterpret_cast<LevelArgs*>(w.largs.p);
         const int nlev = static_cast<int>(level_starts_.size()) - 1;
+        if (l_persist_) {
+            set_level_args(a, dev, st);
+            launch_levels_persist(dev, l_starts_.p, nlev, st);
+            HEC_CUDA(cudaGetLastError());
+            return;
+        }
         if (!w.levels) {  // capture the level launches once, on a private stream
             cudaStream_t cs = nullptr;
             HEC_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             cudaGraph_t graph = nullptr;
             HEC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            launch_levels(dev, level_starts_.data(), nlev, cs);
+            launch_levels(dev, level_starts_.data(), long_starts_.data(), nlev, cs);
             HEC_CUDA(cudaStreamEndCapture(cs, &graph));
             HEC_CUDA(cudaGraphInstantiate(&w.levels, graph, 0));
             cudaGraphDestroy(graph);

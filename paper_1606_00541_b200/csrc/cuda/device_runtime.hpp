@@ -138,6 +138,11 @@ private:
     TriStats stats_;
     // LEVELS
     std::vector<int> level_starts_;
+    std::vector<int> long_starts_;  // per level, into l_long_rows_
+    DevBuf<int> l_long_rows_;
+    int l_long_min_ = 0;
+    DevBuf<int> l_starts_;  // level_starts_ on the device, for the persistent level kernel
+    bool l_persist_ = false;  // HEC_LEVELS_PERSIST: one cooperative launch instead of per-level launches
     DevBuf<int> l_bidx_, l_xidx_, l_oidx_, l_ell_dep_, l_tail_rp_, l_tail_dep_;
     DevBuf<double> l_ell_val_, l_diag_, l_tail_val_;
     int l_width_ = 0, l_ld_ = 0;

@@ -20,9 +20,11 @@ struct LevelArgs {
     const int* tail_rp;
     const int* tail_dep;
     const double* tail_val;
+    const int* long_rows;   // rows with >= long_min remainder entries (a warp each)
     int width;
     int ld;
     int b_ordered;          // b already in reordered-row order (bidx ignored)
+    int long_min;           // 0: every row thread-serial
 };
 
 struct WaveArgs {
@@ -70,8 +72,11 @@ void* cols_kernel(int warps, int rpl, bool unit, bool trace, int order);
 constexpr int kColOrderZYX = 2 | 1 << 2 | 0 << 4;  // (z-1, y-1, x-1): natural-order 7-point factors
 
 // one launch per level, arguments read from dev_args (capturable once, replayed for any vectors)
-void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, int nlev, cudaStream_t st);
+void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, const int* long_starts_host, int nlev,
+                   cudaStream_t st);
 void set_level_args(const LevelArgs& a, LevelArgs* dev, cudaStream_t st);
+// all levels in one cooperative launch with a grid barrier between them
+void launch_levels_persist(const LevelArgs* dev_args, const int* level_starts_dev, int nlev, cudaStream_t st);
 // kernel for sliced-ELL width W (one of 1-8, 10, 13, 16) and solver shape
 // (group warps G x groups K x rpl rows per lane, see wave_inst.cuh); nullptr
 // when that combination is not instantiated

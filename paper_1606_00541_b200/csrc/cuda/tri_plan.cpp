@@ -237,7 +237,7 @@ void validate(const TriSource& s) {
     }
 }
 
-LevelLayout build_levels(const TriSource& s) {
+LevelLayout build_levels(const TriSource& s, int long_min) {
     LevelLayout L;
     L.n = s.n;
     L.ld = round_up(std::max(s.n, 1), 32);
@@ -274,6 +274,15 @@ LevelLayout build_levels(const TriSource& s) {
         }
         L.diag[r] = s.csr_vals[s.csr_rp[r + 1] - 1];
     }
+    L.long_min = std::max(0, long_min);
+    L.long_starts.assign(static_cast<std::size_t>(s.nlev) + 1, 0);
+    for (int k = 0; k < s.nlev; ++k) {
+        if (L.long_min > 0)
+            for (int r = s.level_starts[k]; r < s.level_starts[k + 1]; ++r)
+                if (L.tail_rp[r + 1] - L.tail_rp[r] >= L.long_min) L.long_rows.push_back(r);
+        L.long_starts[k + 1] = static_cast<int>(L.long_rows.size());
+    }
+    if (L.long_rows.empty()) L.long_min = 0;
     return L;
 }
 

@@ -49,8 +49,13 @@ struct LevelLayout {
     std::vector<double> diag;                // n
     std::vector<int> tail_rp, tail_dep;      // CSR remainder without the diagonal
     std::vector<double> tail_val;
+    // rows whose CSR remainder has >= long_min entries, level by level: solved by
+    // a warp each (parallel loads and products, the differences in stored order)
+    int long_min = 0;                        // 0: no warp rows
+    std::vector<int> long_rows, long_starts; // long_starts: nlev + 1
 };
-LevelLayout build_levels(const TriSource& s);
+constexpr int kLongRowMin = 32;  // measured: 40-entry remainders 0.42 -> 0.19 ms (tools/long_rows.py)
+LevelLayout build_levels(const TriSource& s, int long_min = kLongRowMin);
 
 // ------------------------------------------------------------------ WAVE ----
 // Persistent wavefront kernel (one CTA per SM, cooperative launch so every

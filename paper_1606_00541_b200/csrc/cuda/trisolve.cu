@@ -19,10 +19,13 @@
 //                   robin with a named-barrier handoff. The reference's per-level
 //                   barrier becomes dataflow; no grid barrier.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+
+namespace cg = cooperative_groups;
 
 #include "wave_kernel.cuh"
 
@@ -38,17 +41,17 @@ __device__ __forceinline__ double sub_prod(double acc, double v, double x) {
 // so the whole sequence of launches is captured once in a CUDA graph per stream
 // and replayed for any vectors: one argument-setting kernel + one graph launch
 // per solve instead of one launch per level.
-__global__ void k_level_rows(const LevelArgs* __restrict__ pa, int r0, int r1) {
-    const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= r1) return;
-    const LevelArgs& a = *pa;
+__device__ __forceinline__ double level_acc(const LevelArgs& a, int r) {
     double acc = a.b[a.b_ordered ? r : a.bidx[r]];
     for (int k = 0; k < a.width; ++k) {
         const size_t slot = static_cast<size_t>(k) * a.ld + r;
         const int d = a.ell_dep[slot];
         if (d >= 0) acc = sub_prod(acc, a.ell_val[slot], a.xs[d]);
     }
-    for (int t = a.tail_rp[r]; t < a.tail_rp[r + 1]; ++t) acc = sub_prod(acc, a.tail_val[t], a.xs[a.tail_dep[t]]);
+    return acc;
+}
+
+__device__ __forceinline__ void level_store(const LevelArgs& a, int r, double acc) {
     const double x = __ddiv_rn(acc, a.diag[r]);
     a.xs[a.xidx[r]] = x;
     if (a.out) {
@@ -57,18 +60,93 @@ __global__ void k_level_rows(const LevelArgs* __restrict__ pa, int r0, int r1) {
     }
 }
 
+// One row per thread; rows with a long remainder are left to level_row_warp
+// when skip_long.
+__device__ __forceinline__ void level_row(const LevelArgs& a, int r, bool skip_long) {
+    const int t0 = a.tail_rp[r], t1 = a.tail_rp[r + 1];
+    if (skip_long && a.long_min > 0 && t1 - t0 >= a.long_min) return;
+    double acc = level_acc(a, r);
+    for (int t = t0; t < t1; ++t) acc = sub_prod(acc, a.tail_val[t], a.xs[a.tail_dep[t]]);
+    level_store(a, r, acc);
+}
+
+// One row per warp (the remainder loop at triangular.cpp:123-125 for long rows):
+// the lanes load 32 (dep, value) pairs and gather x in parallel and form the
+// products (each rounded on its own, as in sub_prod); the differences then run
+// in stored order on a broadcast accumulator, so the result is the
+// thread-serial one bit for bit. The next 32 entries are in flight meanwhile.
+__device__ __forceinline__ void level_row_warp(const LevelArgs& a, int r, int lane) {
+    const int t0 = a.tail_rp[r], t1 = a.tail_rp[r + 1];
+    double acc = level_acc(a, r);  // every lane the same (broadcast loads)
+    auto prod = [&](int t) { return t < t1 ? __dmul_rn(a.tail_val[t], a.xs[a.tail_dep[t]]) : 0.0; };
+    double p = prod(t0 + lane);
+    for (int t = t0; t < t1; t += 32) {
+        const double pn = prod(t + 32 + lane);
+        const int m = min(32, t1 - t);
+        for (int q = 0; q < m; ++q) acc = __dsub_rn(acc, __shfl_sync(0xffffffffu, p, q));
+        p = pn;
+    }
+    if (lane == 0) level_store(a, r, acc);
+}
+
+// blocks [0, row_blocks) take the level's rows a thread each, the blocks after
+// them its long rows [l0, l1) a warp each.
+__global__ void k_level_rows(const LevelArgs* __restrict__ pa, int r0, int r1, int l0, int l1, int row_blocks) {
+    const LevelArgs& a = *pa;
+    if (static_cast<int>(blockIdx.x) < row_blocks) {
+        const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+        if (r < r1) level_row(a, r, true);
+        return;
+    }
+    const int w = l0 + ((blockIdx.x - row_blocks) * blockDim.x + threadIdx.x) / 32;
+    if (w < l1) level_row_warp(a, a.long_rows[w], threadIdx.x & 31);
+}
+
+// All levels in one cooperative launch, a grid-wide barrier between them (the
+// reference's per-level barrier, triangular.cpp:128, as a grid barrier instead of
+// a kernel boundary): the measured alternative to the per-level launches.
+__global__ void __launch_bounds__(256) k_level_persist(const LevelArgs* __restrict__ pa,
+                                                       const int* __restrict__ level_starts, int nlev) {
+    cg::grid_group grid = cg::this_grid();
+    const LevelArgs& a = *pa;
+    const int stride = gridDim.x * blockDim.x;
+    for (int k = 0; k < nlev; ++k) {
+        const int r1 = level_starts[k + 1];
+        for (int r = level_starts[k] + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += stride)
+            level_row(a, r, false);
+        if (k + 1 < nlev) grid.sync();
+    }
+}
+
+void launch_levels_persist(const LevelArgs* dev_args, const int* level_starts_dev, int nlev, cudaStream_t st) {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_level_persist, 256, 0);
+        blocks = std::max(1, sms * std::max(1, per));
+    }
+    void* args[] = {const_cast<LevelArgs**>(&dev_args), const_cast<int**>(&level_starts_dev), &nlev};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(&k_level_persist), dim3(blocks), dim3(256), args, 0, st);
+}
+
 __global__ void k_set_level_args(LevelArgs a, LevelArgs* dst) { *dst = a; }
 
 void set_level_args(const LevelArgs& a, LevelArgs* dev, cudaStream_t st) {
     k_set_level_args<<<1, 1, 0, st>>>(a, dev);
 }
 
-void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, int nlev, cudaStream_t st) {
+void launch_levels(const LevelArgs* dev_args, const int* level_starts_host, const int* long_starts_host, int nlev,
+                   cudaStream_t st) {
     for (int k = 0; k < nlev; ++k) {
         const int r0 = level_starts_host[k], r1 = level_starts_host[k + 1];
+        const int l0 = long_starts_host[k], l1 = long_starts_host[k + 1];
         const int m = r1 - r0;
         const int tpb = m >= 256 ? 256 : (m >= 128 ? 128 : 64);
-        k_level_rows<<<(m + tpb - 1) / tpb, tpb, 0, st>>>(dev_args, r0, r1);
+        const int row_blocks = (m + tpb - 1) / tpb;
+        const int long_blocks = ((l1 - l0) * 32 + tpb - 1) / tpb;
+        k_level_rows<<<row_blocks + long_blocks, tpb, 0, st>>>(dev_args, r0, r1, l0, l1, row_blocks);
     }
 }
 

@@ -114,6 +114,52 @@ def test_ilut_long_rows(H, orc):
             assert bits_equal(got, want)
 
 
+def _arrow_factor(n, long_every, long_len, rng, upper=False):
+    # three bands of rows; band 1 and 2 rows depend on 3 rows of the band before,
+    # every long_every-th row on long_len rows of the earlier bands (and one row
+    # whose remainder is not a multiple of the warp width)
+    band, rows = n // 3, []
+    for i in range(n):
+        k = min(i // band, 2)
+        if k == 0:
+            cols = np.zeros(0, int)
+        else:
+            m = long_len + (i % 7) if i % long_every == 0 else 3
+            pool = k * band if m > 3 else band
+            cols = np.unique(rng.integers(0, pool, m) + (0 if m > 3 else (k - 1) * band))
+        rows.append((cols, rng.uniform(-1, 1, cols.size) / max(cols.size, 1)))
+    from util import _csr_from_rows
+    full = [(np.append(c, i), np.append(v, 1.5 + rng.uniform())) for i, (c, v) in enumerate(rows)]
+    a = _csr_from_rows(n, full)
+    if not upper:
+        return a
+    # the mirror image is upper triangular: row i -> n-1-i
+    mir = [(n - 1 - c[::-1], v[::-1]) for c, v in full[::-1]]
+    return _csr_from_rows(n, mir)
+
+
+@pytest.mark.parametrize("long_min", ["", "0", "1", "200"])
+@pytest.mark.parametrize("upper", [False, True])
+def test_warp_rows_bitwise(H, orc, monkeypatch, long_min, upper):
+    # level launches: rows with long CSR remainders solved a warp each (products
+    # in parallel, differences in stored order) equal the thread-serial loop of
+    # the reference bit for bit; HEC_LEVELS_LONG moves the threshold (0 = off)
+    if long_min:
+        monkeypatch.setenv("HEC_LEVELS_LONG", long_min)
+    rng = np.random.default_rng(211 + upper)
+    t = _arrow_factor(6000, 37, 700, rng, upper)
+    p = (H.prepare_upper if upper else H.prepare_lower)(to_product(H, t))
+    b = rng.uniform(-1, 1, t.n_rows)
+    b[::97] = -0.0
+    want = orc.solve(orc.prepare(t, upper=upper), b)
+    got, info = device_solve(H, p, b, 1)
+    assert info["strategy"] == 1
+    assert bits_equal(got, want)
+    monkeypatch.setenv("HEC_LEVELS_PERSIST", "1")  # one cooperative launch, grid barrier per level
+    got, _ = device_solve(H, p, b, 1)
+    assert bits_equal(got, want)
+
+
 def test_repeated_and_device_pointer_solves(H, orc):
     torch = pytest.importorskip("torch")
     a = H.gen_poisson7(32, 32, 32)
