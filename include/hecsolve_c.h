@@ -185,6 +185,10 @@ int hec_precond_create_local(int n_in, int n_out, int n_ext, const int* gather, 
                              const int* u_csr_cols, const double* u_csr_vals,
                              const hec_tri_options* options, hec_precond_t* out);
 int hec_precond_apply(hec_precond_t m, const double* r_dev, double* x_dev, void* stream);
+/* Host vectors (pinned for full PCIe speed). Square preconditioners of at least
+ * 2^21 rows copy in slices: each input slice is permuted while the next is in
+ * flight and each output slice copied back while the next is permuted
+ * (HEC_HOST_SLICES overrides the count, 1 = one copy each way). */
 int hec_precond_apply_host(hec_precond_t m, const double* r, double* x);
 int hec_precond_query(hec_precond_t m, hec_tri_info* l_info, hec_tri_info* u_info);
 int hec_precond_destroy(hec_precond_t m);

@@ -422,6 +422,18 @@ void DeviceTri::permute_out(const double* xw, double* xs, cudaStream_t st) const
     HEC_CUDA(cudaGetLastError());
 }
 
+void DeviceTri::scatter_in(const double* b, double* bp, int o0, int o1, cudaStream_t st) const {
+    if (o1 <= o0) return;
+    scatter_rows(b + o0, p_wpos_.p + o0, bp, o1 - o0, st);
+    HEC_CUDA(cudaGetLastError());
+}
+
+void DeviceTri::permute_out_range(const double* xw, double* xs, int o0, int o1, cudaStream_t st) const {
+    if (o1 <= o0) return;
+    permute_in(xw, p_wpos_.p + o0, xs + o0, o1 - o0, st);
+    HEC_CUDA(cudaGetLastError());
+}
+
 void DeviceTri::run_levels(const double* b, bool ordered, double* xs, double* out, cudaStream_t st) {
     {
         LevelArgs a{};
@@ -596,6 +608,12 @@ void DevicePrecond::build_upper(const plan::TriSource& u, const TriOptions& opt)
 
 DevicePrecond::~DevicePrecond() {
     if (h_stream_) cudaStreamDestroy(h_stream_);
+    if (h_in_) cudaStreamDestroy(h_in_);
+    if (h_out_) cudaStreamDestroy(h_out_);
+    for (int k = 0; k < kMaxSlices; ++k) {
+        if (ev_in_[k]) cudaEventDestroy(ev_in_[k]);
+        if (ev_out_[k]) cudaEventDestroy(ev_out_[k]);
+    }
 }
 
 DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
@@ -620,6 +638,11 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
     // right-hand side is gathered straight from there through the composed map
     // (no pass through the solution order in between)
     l_->permute(r, w.bl.p, st);
+    if (identity_) {
+        apply_middle(w.bl.p, w.xw.p, w, st);
+        u_->permute_out(w.xw.p, x, st);
+        return;
+    }
     l_->solve_wave(w.bl.p, w.yw.p, nullptr, st);
     const double* bu = w.yw.p;  // mirrored U: L's output as it lies
     if (!u_->mirrored()) {
@@ -627,12 +650,26 @@ void DevicePrecond::apply(const double* r, double* x, cudaStream_t st) {
         HEC_CUDA(cudaGetLastError());
         bu = w.bu.p;
     }
-    if (identity_) {
-        u_->solve_wave(bu, w.xw.p, nullptr, st);
-        u_->permute_out(w.xw.p, x, st);
-    } else {
-        u_->solve_wave(bu, w.xw.p, x, st);  // owned rows scattered into x by the kernel
+    u_->solve_wave(bu, w.xw.p, x, st);  // owned rows scattered into x by the kernel
+}
+
+// L from its reordered input, then U, output left in U's wave order (square form)
+void DevicePrecond::apply_middle(const double* bl, double* xw, Workspace& w, cudaStream_t st) {
+    l_->solve_wave(bl, w.yw.p, nullptr, st);
+    const double* bu = w.yw.p;  // mirrored U: L's output as it lies
+    if (!u_->mirrored()) {
+        permute_in(w.yw.p, lu_map_.p, w.bu.p, static_cast<int>(u_->wave_len()), st);
+        HEC_CUDA(cudaGetLastError());
+        bu = w.bu.p;
     }
+    u_->solve_wave(bu, xw, nullptr, st);
+}
+
+// slices of at least 2^20 rows (a few microseconds of permutation each), at most 8
+int DevicePrecond::host_slices() const {
+    if (!identity_ || n_ != n_out_ || !l_->sliceable() || !u_->sliceable()) return 1;
+    if (std::getenv("HEC_HOST_SLICES")) return std::max(1, std::min(kMaxSlices, std::atoi(std::getenv("HEC_HOST_SLICES"))));
+    return std::max(1, std::min(kMaxSlices, n_ >> 20));
 }
 void DevicePrecond::compose() {
     const std::vector<int>& bu = u_->host_bidx();
@@ -659,10 +696,43 @@ void DevicePrecond::apply_host(const double* r, double* x) {
     if (!h_stream_) HEC_CUDA(cudaStreamCreateWithFlags(&h_stream_, cudaStreamNonBlocking));
     if (h_r_.count < static_cast<std::size_t>(std::max(n_, 1))) h_r_.alloc(std::max(n_, 1));
     if (h_x_.count < static_cast<std::size_t>(std::max(n_out_, 1))) h_x_.alloc(std::max(n_out_, 1));
-    HEC_CUDA(cudaMemcpyAsync(h_r_.p, r, sizeof(double) * n_, cudaMemcpyHostToDevice, h_stream_));
-    apply(h_r_.p, h_x_.p, h_stream_);
-    HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, sizeof(double) * n_out_, cudaMemcpyDeviceToHost, h_stream_));
-    HEC_CUDA(cudaStreamSynchronize(h_stream_));
+    const int S = host_slices();
+    if (S <= 1) {
+        HEC_CUDA(cudaMemcpyAsync(h_r_.p, r, sizeof(double) * n_, cudaMemcpyHostToDevice, h_stream_));
+        apply(h_r_.p, h_x_.p, h_stream_);
+        HEC_CUDA(cudaMemcpyAsync(x, h_x_.p, sizeof(double) * n_out_, cudaMemcpyDeviceToHost, h_stream_));
+        HEC_CUDA(cudaStreamSynchronize(h_stream_));
+        return;
+    }
+    // the copies dominate (2 x 8n bytes over PCIe against ~1 ms of solves at 256^3):
+    // each input slice is permuted while the next one is in flight, and each
+    // output slice is copied back while the next one is permuted
+    if (!h_in_) {
+        HEC_CUDA(cudaStreamCreateWithFlags(&h_in_, cudaStreamNonBlocking));
+        HEC_CUDA(cudaStreamCreateWithFlags(&h_out_, cudaStreamNonBlocking));
+        for (int k = 0; k < kMaxSlices; ++k) {
+            HEC_CUDA(cudaEventCreateWithFlags(&ev_in_[k], cudaEventDisableTiming));
+            HEC_CUDA(cudaEventCreateWithFlags(&ev_out_[k], cudaEventDisableTiming));
+        }
+    }
+    Workspace& w = workspace(h_stream_);
+    const int step = ((n_ + S - 1) / S + 3) & ~3;  // slice starts stay 16-byte aligned
+    for (int k = 0; k < S; ++k) {
+        const int o0 = std::min(n_, k * step), o1 = std::min(n_, o0 + step);
+        HEC_CUDA(cudaMemcpyAsync(h_r_.p + o0, r + o0, sizeof(double) * (o1 - o0), cudaMemcpyHostToDevice, h_in_));
+        HEC_CUDA(cudaEventRecord(ev_in_[k], h_in_));
+        HEC_CUDA(cudaStreamWaitEvent(h_stream_, ev_in_[k], 0));
+        l_->scatter_in(h_r_.p, w.bl.p, o0, o1, h_stream_);
+    }
+    apply_middle(w.bl.p, w.xw.p, w, h_stream_);
+    for (int k = 0; k < S; ++k) {
+        const int o0 = std::min(n_, k * step), o1 = std::min(n_, o0 + step);
+        u_->permute_out_range(w.xw.p, h_x_.p, o0, o1, h_stream_);
+        HEC_CUDA(cudaEventRecord(ev_out_[k], h_stream_));
+        HEC_CUDA(cudaStreamWaitEvent(h_out_, ev_out_[k], 0));
+        HEC_CUDA(cudaMemcpyAsync(x + o0, h_x_.p + o0, sizeof(double) * (o1 - o0), cudaMemcpyDeviceToHost, h_out_));
+    }
+    HEC_CUDA(cudaStreamSynchronize(h_out_));
 }
 
 }  // namespace hec::dev

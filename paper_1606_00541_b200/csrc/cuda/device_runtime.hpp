@@ -95,6 +95,12 @@ public:
     void solve_wave(const double* bp, double* xw, double* out, cudaStream_t st,
                     unsigned long long* trace = nullptr);
     void permute_out(const double* xw, double* xs, cudaStream_t st) const;
+    // The permutations restricted to the solution indices [o0, o1) (o0 a multiple
+    // of 4), for host copies sliced to overlap them: bp[wpos[o]] = b[o] and
+    // xs[o] = xw[wpos[o]]. Only for wave layouts whose positions are the n rows.
+    bool sliceable() const { return strategy_ == 2 && !cols_ && wave_len_ == n_ && !h_wpos_.empty(); }
+    void scatter_in(const double* b, double* bp, int o0, int o1, cudaStream_t st) const;
+    void permute_out_range(const double* xw, double* xs, int o0, int o1, cudaStream_t st) const;
     // host copies of the maps: bidx (reordered input) and wpos (solution index ->
     // output position; empty = identity)
     const std::vector<int>& host_bidx() const { return h_bidx_; }
@@ -216,6 +222,13 @@ private:
     std::mutex h_mu_;
     DevBuf<double> h_r_, h_x_;
     cudaStream_t h_stream_ = nullptr;
+    // apply_host with the copies sliced: host->device slices on h_in_, the
+    // permutation of each slice on h_stream_ behind it, device->host on h_out_
+    static constexpr int kMaxSlices = 8;
+    cudaStream_t h_in_ = nullptr, h_out_ = nullptr;
+    cudaEvent_t ev_in_[kMaxSlices] = {}, ev_out_[kMaxSlices] = {};
+    int host_slices() const;
+    void apply_middle(const double* bl, double* xw, Workspace& w, cudaStream_t st);
     Workspace& workspace(cudaStream_t st);
 
 public:

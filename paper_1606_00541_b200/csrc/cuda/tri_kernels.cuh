@@ -83,6 +83,8 @@ void launch_levels_persist(const LevelArgs* dev_args, const int* level_starts_de
 void* wave_kernel(int width, int group, int groups, int rpl, bool trace);
 // bp[r] = b[bidx[r]] for r < n (the reference's permute-in pass, coalesced writes)
 void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_t st);
+// bp[wpos[o]] = b[o], o in [0, n)
+void scatter_rows(const double* b, const int* wpos, double* bp, int n, cudaStream_t st);
 constexpr int kWaveSolverWarps = 16;
 // producer / waiter warps of k_wave: 2 + 5 in general (3 waiters could not keep
 // up with 27-point halos); the narrow-row shapes with more groups (z-pencils:

@@ -189,6 +189,24 @@ void permute_in(const double* b, const int* bidx, double* bp, int n, cudaStream_
     k_permute_in4<<<blocks, 256, 0, st>>>(b, bidx, bp, n);
 }
 
+// bp[wpos[o]] = b[o]: the inverse of the gather above, for a slice of the input
+// that has just arrived (coalesced reads, one scattered store per row)
+__global__ void __launch_bounds__(256) k_scatter_rows(const double* __restrict__ b, const int* __restrict__ wpos,
+                                                      double* __restrict__ bp, int n) {
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) bp[__ldcs(wpos + o)] = __ldcs(b + o);
+}
+
+void scatter_rows(const double* b, const int* wpos, double* bp, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    k_scatter_rows<<<std::min((n + 255) / 256, sms * 8), 256, 0, st>>>(b, wpos, bp, n);
+}
+
 // the k_wave instantiations live in wave_inst_*.cu (compiled in parallel)
 void* wave_kernel_a(int width, int group, int groups, int rpl, bool trace);
 void* wave_kernel_b(int width, int group, int groups, int rpl, bool trace);

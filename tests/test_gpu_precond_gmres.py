@@ -45,6 +45,24 @@ def test_apply_vs_oracle(H, orc, strategy):
             assert bits_equal(dp.apply_host(r), want), (kind, blocks, overlap)
 
 
+@pytest.mark.parametrize("slices", ["1", "2", "3", "8"])
+@pytest.mark.parametrize("dims", [(40, 38, 36), (33, 17, 9)])
+def test_apply_host_sliced_copies(H, orc, monkeypatch, slices, dims):
+    # hec_precond_apply_host with the host copies cut into slices (each input
+    # slice permuted while the next is in flight, each output slice copied back
+    # while the next is permuted; default: 2^20 rows a slice, at most 8) gives
+    # the unsliced result bit for bit, for row counts that do not divide evenly
+    monkeypatch.setenv("HEC_HOST_SLICES", slices)
+    a = H.gen_reservoir7(*dims, seed=3)
+    f = H.ilu0(a)
+    b = np.random.default_rng(17).uniform(-1, 1, a.n_rows)
+    y = orc.solve(orc.prepare(to_oracle(f.l)), b)
+    want = orc.solve(orc.prepare(to_oracle(f.u), upper=True), y)
+    dp = H.DevicePrecond.create(a.n_rows, H.prepare_lower(f.l), H.prepare_upper(f.u))
+    for _ in range(2):  # the slice streams and events are reused
+        assert bits_equal(dp.apply_host(b), want)
+
+
 def to_oracle_prep(orc, p):
     from oracle.oracle import Prepared
     s, e = p.schedule, p.hec
