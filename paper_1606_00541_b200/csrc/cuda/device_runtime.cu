@@ -623,8 +623,9 @@ DevicePrecond::Workspace& DevicePrecond::workspace(cudaStream_t st) {
         w = std::make_unique<Workspace>();
         const std::size_t ll = static_cast<std::size_t>(std::max<long long>(l_->wave_len(), 1));
         const std::size_t lu = static_cast<std::size_t>(std::max<long long>(u_->wave_len(), 1));
+        // k_wave inputs: bulk copies of b read up to one element past the last row
         w->bl.alloc(ll + 2);
-        w->yw.alloc(ll);
+        w->yw.alloc(ll + 2);  // also U's input when U mirrors L
         w->bu.alloc(lu + 2);
         w->xw.alloc(lu);
     }
