@@ -207,6 +207,30 @@ __global__ void k_pack(int m, const int* __restrict__ idx, const double* v, doub
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) send[i] = v[idx[i]];
 }
 
+struct PinnedHost {
+    double* p = nullptr;
+    explicit PinnedHost(std::size_t n) { HEC_CUDA(cudaMallocHost(&p, sizeof(double) * std::max<std::size_t>(n, 1))); }
+    ~PinnedHost() {
+        if (p) cudaFreeHost(p);
+    }
+    PinnedHost(const PinnedHost&) = delete;
+    PinnedHost& operator=(const PinnedHost&) = delete;
+};
+
+struct EventPair {
+    cudaEvent_t e[2] = {};
+    EventPair() {
+        for (auto& x : e) HEC_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    ~EventPair() {
+        for (auto& x : e)
+            if (x) cudaEventDestroy(x);
+    }
+    cudaEvent_t operator[](int k) const { return e[k]; }
+    EventPair(const EventPair&) = delete;
+    EventPair& operator=(const EventPair&) = delete;
+};
+
 int sm_count() {
     int dev = 0, sms = 0;
     HEC_CUDA(cudaGetDevice(&dev));
@@ -296,7 +320,16 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     HEC_CUDA(cudaMemcpyAsync(b.p, b_own, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     double* hb1 = hb.p;            // pass-1 dots (j+1)
     double* hb2 = hb.p + mr + 2;   // pass-2 dots (j+1), ||w'||^2, ||w''||
-    std::vector<double> hh(2 * static_cast<size_t>(mr) + 8);
+    // pinned host staging for the per-iteration Hessenberg column and the other
+    // small host round trips: a copy into pageable memory goes through the
+    // driver's staging buffer, synchronously (measured: 256^3 solves of 1.34 to
+    // 2.04 s for the same 1.28 s of device phases)
+    const size_t hstride = 2 * static_cast<size_t>(mr) + 8;
+    PinnedHost hpin(2 * hstride + (mr + 1) + 1);
+    double* const hh2 = hpin.p;  // two slots: column j read while column j+1 runs
+    double* const ny = hpin.p + 2 * hstride;
+    double* const s2p = ny + mr + 1;
+    EventPair ev_col;
 
     auto halo = [&](double* vloc) {  // fill vloc[n_own ..) from the owners
         if (comm.world() == 1) return;
@@ -354,15 +387,17 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     auto norm = [&](const double* v) {  // sqrt(sum over ranks of v . v)
         mv(0, nullptr, nullptr, v, nullptr, 0, 1.0, nullptr, 1, 1, hb.p);
         comm.allreduce_sum(hb.p, 1, st);
-        double s2 = 0.0;
-        HEC_CUDA(cudaMemcpyAsync(&s2, hb.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        HEC_CUDA(cudaMemcpyAsync(s2p, hb.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         HEC_CUDA(cudaStreamSynchronize(st));
-        return std::sqrt(s2);
+        return std::sqrt(*s2p);
     };
 
     const double bnorm = norm(b.p);
+    if (prof.on)
+        std::fprintf(stderr, "[hec gmres] setup (buffers, first norm) %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     const double threshold = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
-    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr), ny(mr + 1);
+    std::vector<double> h(static_cast<size_t>(mr + 1) * mr, 0.0), cs(mr), sn(mr), g(mr + 1), y(mr);
     HEC_CUDA(cudaMemcpyAsync(r.p, b.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
     double rnorm = bnorm;
     bool stalled = false;
@@ -378,14 +413,14 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = rnorm;
 
-        int j = 0;
-        bool lucky = false;
-        while (j < mr && out.iterations < cfg.max_iters) {
-            double* vj = V.p + j * ldv;
+        // Column jj of the Arnoldi process: apply, the Gram-Schmidt passes, and
+        // the copy of its Hessenberg entries into host slot jj & 1 (event ev_col).
+        auto launch_col = [&](int jj) {
+            double* vj = V.p + jj * ldv;
             prof.mark(st, 0);
             apply_op(vj, w.p);
             prof.mark(st, 1);
-            const int kc = j + 1;
+            const int kc = jj + 1;
             if (kc <= kKG) {
                 // CGS2 pass 1: h1 = V^T w
                 mv(kc, V.p, nullptr, w.p, nullptr, 0, 1.0, nullptr, 1, 0, hb1);
@@ -395,8 +430,8 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
                 mv(kc, V.p, hb1, w.p, w.p, 0, 1.0, nullptr, 1, 1, hb2);
                 prof.mark(st, 3);
                 comm.allreduce_sum(hb2, kc + 1, st);
-                // v_{j+1} = (w' - V h2) / ||w''||
-                mv(kc, V.p, hb2, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
+                // v_{jj+1} = (w' - V h2) / ||w''||
+                mv(kc, V.p, hb2, w.p, V.p + (jj + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
                 prof.mark(st, 4);
             } else {
                 // more basis vectors than one fused pass holds: modified Gram-Schmidt,
@@ -408,10 +443,26 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
                 }
                 comm.allreduce_sum(hb2 + kc, 1, st);
                 HEC_CUDA(cudaMemsetAsync(hb2, 0, sizeof(double) * kc, st));
-                mv(0, nullptr, hb2 + kc, w.p, V.p + (j + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
+                mv(0, nullptr, hb2 + kc, w.p, V.p + (jj + 1) * ldv, 2, 1.0, hb2 + kc + 1, 0, 0, nullptr);
             }
-            HEC_CUDA(cudaMemcpyAsync(hh.data(), hb.p, sizeof(double) * (2 * mr + 8), cudaMemcpyDeviceToHost, st));
-            HEC_CUDA(cudaStreamSynchronize(st));
+            HEC_CUDA(cudaMemcpyAsync(hh2 + (jj & 1) * hstride, hb.p, sizeof(double) * (2 * mr + 8),
+                                     cudaMemcpyDeviceToHost, st));
+            HEC_CUDA(cudaEventRecord(ev_col[jj & 1], st));
+        };
+        // The next column only needs v_{j+1}, which the device produces itself, so
+        // it is queued before the host reads column j's entries: the host's Givens
+        // work and its wake-up latency hide behind a column of device work. If the
+        // cycle stops at column j (convergence or breakdown), the queued column is
+        // discarded (it touches neither h, g nor V[:, <= j+1]).
+        const bool ahead = !prof.on;  // the phase profile wants one column at a time
+        int j = 0;
+        bool lucky = false;
+        if (j < mr && out.iterations < cfg.max_iters) launch_col(0);
+        while (j < mr && out.iterations < cfg.max_iters) {
+            const int kc = j + 1;
+            if (ahead && j + 1 < mr && out.iterations + 1 < cfg.max_iters) launch_col(j + 1);
+            HEC_CUDA(cudaEventSynchronize(ev_col[j & 1]));
+            const double* hh = hh2 + (j & 1) * hstride;
             prof.collect();
             for (int i = 0; i <= j; ++i) h[i + j * (mr + 1)] = hh[i] + hh[mr + 2 + i];
             const double hjj1 = hh[mr + 2 + kc + 1];
@@ -445,6 +496,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
             const double est = std::fabs(g[j]);
             out.inner_residuals.push_back(est);
             if (est <= threshold || lucky) break;
+            if (!ahead && j < mr && out.iterations < cfg.max_iters) launch_col(j);
         }
 
         // back substitution (gmres.cpp:113-119), x += M^-1 (V y), r = b - A x
@@ -455,7 +507,7 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         }
         // xc = sum_i y_i V_i from 0.0 in i order (gmres.cpp:121-122) as 0 - sum (-y_i) V_i (exact negation)
         for (int i = 0; i < j; ++i) ny[i] = -y[i];
-        HEC_CUDA(cudaMemcpyAsync(yv.p, ny.data(), sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
+        HEC_CUDA(cudaMemcpyAsync(yv.p, ny, sizeof(double) * std::max(j, 1), cudaMemcpyHostToDevice, st));
         HEC_CUDA(cudaStreamSynchronize(st));  // ny is reused next cycle
         for (int k0 = 0; k0 < std::max(j, 1); k0 += kKG)  // groups of at most kKG columns, k order kept
             mv(std::min(kKG, j - k0), V.p + k0 * ldv, yv.p + k0, k0 ? xc.p : nullptr, xc.p, 0, 1.0, nullptr, 0, 0,

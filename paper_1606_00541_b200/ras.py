@@ -224,7 +224,7 @@ class RasSolver:
                          ar.value, ex.value, la.value)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # (module globals are gone at interpreter exit)
             lib.hec_ras_destroy(self._h)
         self._h = None
 

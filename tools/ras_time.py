@@ -15,7 +15,7 @@ a = H.gen_poisson7(s, s, s)
 solver = ras.RasSolver(a, overlap=1, comm="none")
 b = torch.tensor(H.spmv_csr(a, np.ones(a.n_rows)), device="cuda")
 x = torch.zeros_like(b)
-for k in range(3):
+for k in range(int(os.environ.get("RAS_REPS", "3"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = solver.gmres_device(b, x, restart=30)
