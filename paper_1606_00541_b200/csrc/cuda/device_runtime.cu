@@ -138,8 +138,9 @@ DeviceTri::DeviceTri(const plan::TriSource& src, const TriOptions& opt, const pl
                 }
             }
             if (!cfg.mirror) P = plan::build_wave(src, cfg);
-        } catch (const std::invalid_argument&) {
+        } catch (const std::invalid_argument& e) {
             ok = false;  // row order the wave layout cannot schedule: level launches
+            if (std::getenv("HEC_DEBUG")) std::fprintf(stderr, "[hec] no wave layout: %s\n", e.what());
         }
         if (cols_) {
             stats_.strategy = strategy_;
