@@ -46,7 +46,7 @@ def test_apply_vs_oracle(H, orc, strategy):
 
 
 @pytest.mark.parametrize("slices", ["1", "2", "3", "8"])
-@pytest.mark.parametrize("dims", [(40, 38, 36), (33, 17, 9)])
+@pytest.mark.parametrize("dims", [(40, 38, 36), (33, 17, 9), (64, 64, 20)])
 def test_apply_host_sliced_copies(H, orc, monkeypatch, slices, dims):
     # hec_precond_apply_host with the host copies cut into slices (each input
     # slice permuted while the next is in flight, each output slice copied back
