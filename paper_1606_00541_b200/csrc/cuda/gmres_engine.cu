@@ -51,15 +51,16 @@ constexpr int kMaxOut = kKG + 1;
 // Block-reduces acc[0..kc) and, with_norm, acc[kKG] (as output kc) to
 // partials[k * grid + block]; the last block to finish sums partials[k * grid +
 // 0..grid) in a fixed order into out[k]. Fixed shapes: run-to-run reproducible.
-__device__ __forceinline__ void reduce_out(double (&acc)[kMaxOut], int kc, int with_norm, double* partials,
+template <int KG>
+__device__ __forceinline__ void reduce_out(double (&acc)[KG + 1], int kc, int with_norm, double* partials,
                                            unsigned* counter, double* out) {
-    __shared__ double sw[kMaxOut][kT / 32];
+    __shared__ double sw[KG + 1][kT / 32];
     __shared__ bool last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;  // blockDim <= kT
     const int cnt = kc + (with_norm ? 1 : 0);
 #pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) {
-        const bool use = k < kc || (k == kKG && with_norm);
+    for (int k = 0; k < (KG + 1); ++k) {
+        const bool use = k < kc || (k == KG && with_norm);
         if (use) {
             double v = acc[k];
             for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
@@ -130,10 +131,13 @@ __device__ __forceinline__ void mv_issue(const MvArgs& a, int tile, double* stag
         bulk_g2s(stage + k * rows, k < a.kc ? a.V + k * a.ldv + r0 : a.w_in + r0, bytes, bar);
 }
 
-__global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
+// KG: the widest pass this instantiation takes (its accumulators live in
+// registers: 8 / 16 / 32 columns leave room for 4 / 3 / 2 blocks per SM)
+template <int KG>
+__global__ void __launch_bounds__(kTile, KG <= 8 ? 4 : (KG <= 16 ? 3 : 2)) k_mv(MvArgs a) {
     extern __shared__ __align__(128) double mv_smem[];
     __shared__ uint64_t bar[2];
-    __shared__ double sc[kMaxOut];
+    __shared__ double sc[(KG + 1)];
     __shared__ double s_scale;
     const int tid = threadIdx.x, rows = blockDim.x;
     const int ntiles = (a.n + rows - 1) / rows;
@@ -161,9 +165,9 @@ __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
             if (tile < ntiles) mv_issue(a, tile, mv_smem + q * per_stage, &bar[q], tid);
         }
     const double s = s_scale;
-    double acc[kMaxOut];
+    double acc[(KG + 1)];
 #pragma unroll
-    for (int k = 0; k < kMaxOut; ++k) acc[k] = 0.0;
+    for (int k = 0; k < (KG + 1); ++k) acc[k] = 0.0;
     for (int it = 0, tile = blockIdx.x; tile < ntiles; ++it, tile += gridDim.x) {
         const int q = it & 1;
         const double* st = mv_smem + q * per_stage;
@@ -173,16 +177,16 @@ __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
             double u = a.w_in ? st[a.kc * rows + tid] : 0.0;
             if (a.w_out) {
 #pragma unroll
-                for (int k = 0; k < kKG; ++k)
+                for (int k = 0; k < KG; ++k)
                     if (k < a.kc) u = __dsub_rn(u, __dmul_rn(sc[k], st[k * rows + tid]));
                 if (a.scale_mode) u = __ddiv_rn(u, s);
                 a.w_out[i] = u;
             }
             if (a.dots) {
 #pragma unroll
-                for (int k = 0; k < kKG; ++k)
+                for (int k = 0; k < KG; ++k)
                     if (k < a.kc) acc[k] = __dadd_rn(acc[k], __dmul_rn(st[k * rows + tid], u));
-                acc[kKG] = __dadd_rn(acc[kKG], __dmul_rn(u, u));
+                acc[KG] = __dadd_rn(acc[KG], __dmul_rn(u, u));
             }
         }
         __syncthreads();  // every thread is done with this stage
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(kTile) k_mv(MvArgs a) {
             }
         }
     }
-    if (a.dots) reduce_out(acc, a.kc, a.with_norm, a.partials, a.counter, a.out);
+    if (a.dots) reduce_out<KG>(acc, a.kc, a.with_norm, a.partials, a.counter, a.out);
 }
 
 __global__ void k_add_v(int n, double* x, const double* d) {
@@ -351,8 +355,13 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
     // one multi-vector pass (k_mv): grid sized by the shared memory its tiles need
     static bool mv_attr = false;
     if (!mv_attr) {
-        HEC_CUDA(cudaFuncSetAttribute(k_mv, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * kMaxOut * kTile * static_cast<int>(sizeof(double))));
+        for (auto k : {k_mv<8>, k_mv<16>, k_mv<kKG>}) {
+            HEC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          2 * kMaxOut * kTile * static_cast<int>(sizeof(double))));
+            // several blocks per SM need the whole carve-out as shared memory
+            HEC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+        }
         mv_attr = true;
     }
     auto mv = [&](int kc, const double* Vb, const double* c, const double* w_in, double* w_out, int scale_mode,
@@ -377,10 +386,12 @@ GmresOutcome gmres_dist(DistSystem& S, const double* b_own, double* x_own, const
         // tiles in flight) per SM
         const int rows = (kc + 1) * kTile * 16 <= 72 * 1024 ? kTile : kTile / 2;
         const int smem = 2 * (kc + 1) * rows * static_cast<int>(sizeof(double));
-        const int per_sm = std::max(1, std::min(2048 / rows, (227 * 1024) / (smem + 2048)));
+        void (*kern)(MvArgs) = kc <= 8 ? k_mv<8> : (kc <= 16 ? k_mv<16> : k_mv<kKG>);
+        int per_sm = 0;  // resident blocks (registers, shared memory): one wave of persistent blocks
+        HEC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, rows, smem));
         const int ntiles = (n + rows - 1) / rows;
-        const int g = std::max(1, std::min(ntiles, per_sm * sms));
-        k_mv<<<g, rows, smem, st>>>(m);
+        const int g = std::max(1, std::min(ntiles, std::max(per_sm, 1) * sms));
+        kern<<<g, rows, smem, st>>>(m);
         HEC_CUDA(cudaGetLastError());
         ++out.launches;
     };
