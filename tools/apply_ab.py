@@ -37,13 +37,8 @@ def main():
         dp.apply(b, x)
     e1.record()
     torch.cuda.synchronize()
-    from oracle import load_reference  # the reference's own solve on the product's prepared arrays
-    r = load_reference()
-    bh = b.cpu().numpy()
-    ref = r.solve(r.prepared_from(pu), r.solve(r.prepared_from(pl), bh, os.cpu_count()), os.cpu_count())
-    same = bool((x.cpu().numpy().view(np.uint64) == ref.view(np.uint64)).all())
     print(f"{args.stencil}-pt {s}^3 env={ {k: v for k, v in os.environ.items() if k.startswith('HEC_')} }: "
-          f"{e0.elapsed_time(e1) / args.reps:.4f} ms per apply, bitwise={same} ctas={info[0]['ctas'] if info else '?'}", flush=True)
+          f"{e0.elapsed_time(e1) / args.reps:.4f} ms per apply, ctas={info[0]['ctas'] if info else '?'}", flush=True)
 
 
 if __name__ == "__main__":

@@ -1,8 +1,8 @@
 """Long CSR rows (diagnostics): lower-triangular factors whose rows mostly have a
 few dependencies but some have thousands (an arrow-like tail, the loop at
 proj/src/triangular.cpp:123-125), solved by the level launches and by the
-wavefront kernel; prints the solve time per strategy and whether the result is
-bitwise equal to the C oracle.
+wavefront kernel; prints the solve time per strategy (bitwise parity of the
+warp rows: tests/test_gpu_trisolve.py::test_warp_rows_bitwise).
 
     python tools/long_rows.py --n 400000 --levels 4 --long-every 256 --long-len 4096
 """
@@ -48,7 +48,6 @@ def main():
     ap.add_argument("--long-every", type=int, default=256)
     ap.add_argument("--long-len", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--check", action="store_true", help="compare with the C oracle (tests/ helper)")
     args = ap.parse_args()
     import torch
     t0 = time.time()
@@ -57,12 +56,6 @@ def main():
     p = H.prepare_lower(m)
     print(f"n {args.n} nnz {len(vv)} levels {p.schedule.nlev} setup {time.time() - t0:.1f} s", flush=True)
     b = np.random.default_rng(1).uniform(-1, 1, args.n)
-    want = None
-    if args.check:
-        from oracle import load_oracle  # the checker (test infrastructure)
-        from oracle.oracle import Csr
-        orc = load_oracle()
-        want = orc.solve(orc.prepare(Csr(args.n, args.n, rp, ci, vv)), b)
     for strategy in (0, 1, 2):  # auto, level launches, wavefront
         try:
             t = H.DeviceTri.create(p, strategy=strategy)
@@ -83,9 +76,7 @@ def main():
             e1.record()
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
-        ok = "" if want is None else (" bitwise" if np.array_equal(x.cpu().numpy().view(np.int64), want.view(np.int64))
-                                      else " MISMATCH")
-        print(f"asked {strategy}: strategy {info['strategy']} layout {info.get('layout')}: {np.median(ms):.4f} ms{ok}", flush=True)
+        print(f"asked {strategy}: strategy {info['strategy']} layout {info.get('layout')}: {np.median(ms):.4f} ms", flush=True)
         del t
 
 
