@@ -160,6 +160,35 @@ def test_warp_rows_bitwise(H, orc, monkeypatch, long_min, upper):
     assert bits_equal(got, want)
 
 
+def test_warp_rows_at_size(H, orc):
+    # 300k rows in three bands, every 256th row of bands 1-2 with ~4000 entries:
+    # the level launches' warp rows at a size where every level spans all SMs
+    rng = np.random.default_rng(5)
+    n, band = 300000, 100000
+    cols, rp = [], [0]
+    for i in range(n):
+        k = i // band
+        if k == 0:
+            c = np.zeros(0, np.int64)
+        elif i % 256 == 0:
+            c = np.unique(rng.integers(0, k * band, 4000))
+        else:
+            c = np.unique(rng.integers((k - 1) * band, k * band, 3))
+        cols.append(c)
+        cols.append(np.array([i]))
+        rp.append(rp[-1] + c.size + 1)
+    ci = np.concatenate(cols).astype(np.int32)
+    v = rng.uniform(-1, 1, ci.size) / 64.0
+    v[np.array(rp[1:]) - 1] = 1.5  # diagonals
+    from oracle.oracle import Csr
+    t = Csr(n, n, np.array(rp, np.int32), ci, v)
+    p = H.prepare_lower(to_product(H, t))
+    b = rng.uniform(-1, 1, n)
+    got, info = device_solve(H, p, b, 1)
+    assert info["strategy"] == 1
+    assert bits_equal(got, orc.solve(orc.prepare(t), b))
+
+
 def test_repeated_and_device_pointer_solves(H, orc):
     torch = pytest.importorskip("torch")
     a = H.gen_poisson7(32, 32, 32)
