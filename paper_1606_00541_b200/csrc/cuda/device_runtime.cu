@@ -561,8 +561,13 @@ DevicePrecond::DevicePrecond(int n_in, int n_out, int n_ext, const int* gather, 
         if (out_index[k] >= 0 && ++hits[out_index[k]] > 1)
             throw std::invalid_argument("hec_precond_create_local: output row written twice");
     }
-    l.b_map = gather;
-    u.out_map = out_index;
+    // identity maps (one subdomain holding the whole vector): the square form
+    identity_ = n_in == n_out && n_ext == n_in;
+    for (int k = 0; identity_ && k < n_ext; ++k) identity_ = gather[k] == k && out_index[k] == k;
+    if (!identity_) {
+        l.b_map = gather;
+        u.out_map = out_index;
+    }
     l_ = std::make_unique<DeviceTri>(l, opt);
     build_upper(u, opt);
 }
@@ -573,6 +578,11 @@ DevicePrecond::DevicePrecond(int n, int n_ext, const int* gather, const char* ow
     require_device();
     identity_ = gather == nullptr;
     if (identity_ && n_ext != n) throw std::invalid_argument("hec_precond_create: identity map needs n_ext == n");
+    if (!identity_ && n_ext == n && owned) {  // one block covering every row in order: the square form
+        bool id = true;
+        for (int k = 0; id && k < n; ++k) id = gather[k] == k && owned[k];
+        identity_ = id;
+    }
     if (l.n != n_ext || u.n != n_ext) throw std::invalid_argument("hec_precond_create: factor size mismatch");
     std::vector<int> out_map;
     if (!identity_) {
