@@ -172,7 +172,10 @@ int hec_precond_create(int n, int n_ext, const int* gather, const char* owned,
  * layer): the input vector has n_in entries and factor row k reads
  * r[gather[k]]; the output has n_out entries and factor row k writes
  * x[out_index[k]] unless out_index[k] < 0 (rows the subdomain does not own).
- * Replaces one block of hec::apply (proj/src/precond.cpp:125-143).
+ * Replaces one block of hec::apply (proj/src/precond.cpp:125-143). Identity
+ * maps (n_in == n_out == n_ext, gather[k] == out_index[k] == k: one subdomain
+ * holding the whole vector) build the same object as hec_precond_create
+ * without maps.
  */
 int hec_precond_create_local(int n_in, int n_out, int n_ext, const int* gather, const int* out_index,
                              /* L */ int l_nlev, const int* l_level_starts, const int* l_inv_perm,
