@@ -28,8 +28,10 @@ def test_apply_matches_reference_golden(H):
         assert bits_equal(H.apply(m, d["r"]), d[f"{tag}_apply"]), tag
 
 
-@pytest.mark.parametrize("strategy", [1, 2])
-def test_apply_vs_oracle(H, orc, strategy):
+@pytest.mark.parametrize("strategy,long_min", [(1, ""), (1, "1"), (2, "")])  # "1": every remainder a warp row
+def test_apply_vs_oracle(H, orc, monkeypatch, strategy, long_min):
+    if long_min:
+        monkeypatch.setenv("HEC_LEVELS_LONG", long_min)
     rng = np.random.default_rng(61)
     mats = [H.gen_poisson7(14, 12, 10), to_product(H, random_diag_dominant(300, 0.02, rng)),
             H.gen_reservoir7(12, 11, 10)]
